@@ -1,0 +1,130 @@
+/*
+ * ff_chain.h -- C ABI of the B200-native fused GEMM-chain runtime.
+ *
+ * This is the drop-in boundary for the execution path of the reference
+ * planner `fuseplan` (arXiv 2512.12949 front-end).  The reference executes a
+ * fusion plan with a numpy tile replay; these entry points execute the same
+ * plan on an sm_100a GPU.  Plain C types only: no torch / no C++ in the
+ * signatures.  All pointers are device pointers unless stated otherwise;
+ * `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Reference interfaces replaced (file:line in /root/reference/pkg/src/fuseplan):
+ *   ff_chain_run_plan      <- simulator.execute_plan      (simulator.py:177-424)
+ *                             (called by simulator.verify  simulator.py:461-487,
+ *                              search refine               search.py:527-536,
+ *                              cli simulate                cli.py:232-249)
+ *   ff_plan_lower          <- plan.plan_geometry           (plan.py:222-268)
+ *                             + structural_violations      (plan.py:271-324)
+ *                             (the plan -> launch geometry step)
+ *   ff_chain_launch        <- the per-cluster replay loop  (simulator.py:276-409)
+ *                             with an explicit physical configuration
+ *   ff_chain_workspace_bytes <- fits_execution_budget      (simulator.py:137-140)
+ *   status codes            <- errors.py:1-61 (PlanError / CapacityExceeded /
+ *                             FusePlanError); never abort the process.
+ */
+#ifndef FF_CHAIN_H
+#define FF_CHAIN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; mapped back to the reference exception classes in Python */
+#define FF_OK 0
+#define FF_ERR_PLAN 1        /* PlanError: structurally invalid plan / rule violation */
+#define FF_ERR_CAPACITY 2    /* CapacityExceeded: does not fit on-chip */
+#define FF_ERR_UNSUPPORTED 3 /* valid plan, but no kernel lowering for it */
+#define FF_ERR_CUDA 4        /* CUDA runtime / driver failure */
+#define FF_ERR_ARG 5         /* bad argument (null pointer, misaligned, ...) */
+
+/* workload.py:26-32 */
+#define FF_KIND_STANDARD 0
+#define FF_KIND_GATED 1
+#define FF_ACT_IDENTITY 0
+#define FF_ACT_RELU 1
+#define FF_ACT_SILU 2
+#define FF_ACT_GELU_TANH 3 /* extension: GPT-2 FFN (not in the reference catalog) */
+
+/* plan.py:27-30 */
+#define FF_LOWERING_NA 0
+#define FF_LOWERING_SPATIAL_SPLIT 1
+#define FF_LOWERING_DOUBLED_K 2
+
+/* ChainGraph (workload.py:75-110): kind, dims (m,n,k,l), activation. */
+typedef struct ffChainDesc {
+  int32_t kind;
+  int32_t activation;
+  int64_t m, n, k, l;
+  int32_t element_size; /* bytes per stored scalar; only 2 (bf16) executes on the GPU */
+} ffChainDesc;
+
+/* FusionPlan (plan.py:121-165).  Dimension index order is (m, n, k, l) = DIMS. */
+typedef struct ffPlanDesc {
+  uint32_t spatial_mask;   /* bit i set <=> DIMS[i] is spatial */
+  int32_t temporal[4];     /* temporal order, outermost first, as DIMS indices */
+  int32_t n_temporal;
+  int64_t block[4];        /* tiles.block */
+  int32_t cluster[4];      /* tiles.cluster: cls_m, cls_n, cls_k, cls_l */
+  int32_t gated_lowering;  /* FF_LOWERING_* */
+} ffPlanDesc;
+
+/* Physical launch configuration produced by the lowering. */
+typedef struct ffKernelConfig {
+  int32_t ring;        /* CTAs per cluster in the shuffle ring (cls_shuffle) */
+  int32_t n_splits;    /* clusters splitting N (inter-cluster reduce when > 1) */
+  int32_t nb;          /* C chunk width per CTA per n-step (columns) */
+  int32_t lb;          /* E columns owned by one CTA (TMEM accumulator width) */
+  int32_t m_tiles;     /* ceil(m / 128) */
+  int32_t l_clusters;  /* l / (ring * lb) */
+  int32_t steps;       /* n-steps per split */
+  int32_t grid_ctas;   /* total CTAs launched */
+} ffKernelConfig;
+
+/* Tensors: row-major, the reference layouts (simulator.py:112-123):
+ * A[m,k], B[k,n] (standard) or B0[k,n], B1[k,n] (gated), D[n,l], E[m,l]. bf16. */
+typedef struct ffTensors {
+  const void* a;
+  const void* b;  /* B (standard) or B0 (gated) */
+  const void* b1; /* B1 (gated), NULL otherwise */
+  const void* d;
+  void* e;
+} ffTensors;
+
+/* Lower a reference plan to a physical launch (no GPU work). */
+int ff_plan_lower(const ffChainDesc* chain, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out);
+
+/* Choose the physical launch for a chain without a reference plan. */
+int ff_auto_config(const ffChainDesc* chain, int32_t num_sms, ffKernelConfig* out);
+
+/* Workspace (device bytes) the launch needs; 0 when none. */
+size_t ff_chain_workspace_bytes(const ffChainDesc* chain, const ffKernelConfig* cfg);
+
+/* Execute the fused chain with an explicit physical configuration.
+ * Stream-ordered, no host synchronisation, no allocation. */
+int ff_chain_launch(const ffChainDesc* chain, const ffKernelConfig* cfg, const ffTensors* t, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* Lower + launch in one call: the drop-in for simulator.execute_plan. */
+int ff_chain_run_plan(const ffChainDesc* chain, const ffPlanDesc* plan, const ffTensors* t, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Debug variant of ff_chain_launch that also writes the bf16 intermediate C[m,n]. */
+int ff_chain_launch_debug(const ffChainDesc* chain, const ffKernelConfig* cfg, const ffTensors* t,
+                          void* workspace, size_t workspace_bytes, void* c_out, void* stream);
+
+/* Number of CUDA kernels one ff_chain_launch issues (for launch accounting). */
+int ff_chain_kernel_count(const ffChainDesc* chain, const ffKernelConfig* cfg);
+
+/* Thread-local message for the last non-OK status. */
+const char* ff_last_error(void);
+
+/* Library version string. */
+const char* ff_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FF_CHAIN_H */

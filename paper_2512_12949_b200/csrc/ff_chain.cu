@@ -1,0 +1,349 @@
+// Host side of the fused-chain runtime: plan lowering, TMA descriptors,
+// launch, and the C ABI declared in include/ff_chain.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ff_chain.h"
+#include "ff_chain_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+// ---------------------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+// ---------------------------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// Row-major bf16 matrix [rows][cols] -> 2-D map with a (box_cols x box_rows) box, 128B swizzle.
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
+              uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int num_sms_cached() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// kernel table
+// ---------------------------------------------------------------------------
+template <bool kGated, int kNB, int kLB>
+struct StagesFor {
+  static constexpr int kBudget = 232448;
+  using Probe = ff::ChainCfg<kGated, kNB, kLB, 1>;
+  static constexpr int kFixed = Probe::kSMEM - Probe::kSTAGE - 2 * 8;  // everything but the stages
+  static constexpr int kMax = (kBudget - kFixed - 64) / (Probe::kSTAGE + 16);
+  static constexpr int value = kMax > 6 ? 6 : kMax;
+};
+
+template <bool kGated, int kNB, int kLB>
+int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
+                void* c_debug, cudaStream_t stream) {
+  constexpr int kStages = StagesFor<kGated, kNB, kLB>::value;
+  static_assert(kStages >= 2, "not enough shared memory for a pipeline");
+  using C = ff::ChainCfg<kGated, kNB, kLB, kStages>;
+  auto kern = ff::ff_chain_kernel<kGated, kNB, kLB, kStages>;
+
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  if (attr_err != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+
+  CUtensorMap mA, mB0, mB1, mD;
+  const uint64_t M = ch->m, N = ch->n, K = ch->k, L = ch->l;
+  bool ok = make_map(&mA, t->a, M, K, 64, 128);
+  ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
+  ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
+  ok = ok && make_map(&mD, t->d, N, L, 64, 64);
+  if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+
+  ff::ChainArgs a;
+  a.M = (int)M;
+  a.N = (int)N;
+  a.K = (int)K;
+  a.L = (int)L;
+  a.G = cfg->ring;
+  a.S = cfg->n_splits;
+  a.steps = cfg->steps;
+  a.m_tiles = cfg->m_tiles;
+  a.l_clusters = cfg->l_clusters;
+  a.act = ch->activation;
+  a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
+  a.ws = reinterpret_cast<float*>(ws);
+  a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
+
+  if (cfg->n_splits > 1) {
+    cudaError_t e = cudaMemsetAsync(ws, 0, (size_t)M * L * sizeof(float), stream);
+    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  }
+
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(cfg->grid_ctas, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = C::kSMEM;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cfg->ring;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, a);
+  if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
+
+  if (cfg->n_splits > 1) {
+    const size_t n = (size_t)M * L;
+    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(ws),
+                                                                      a.E, n);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
+  }
+  return FF_OK;
+}
+
+using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);
+
+LaunchFn select_kernel(bool gated, int nb, int lb) {
+#define FF_CASE(G, NB, LB) \
+  if (gated == G && nb == NB && lb == LB) return &launch_impl<G, NB, LB>;
+  FF_CASE(false, 128, 256)
+  FF_CASE(false, 128, 128)
+  FF_CASE(false, 128, 64)
+  FF_CASE(false, 64, 256)
+  FF_CASE(false, 64, 128)
+  FF_CASE(false, 64, 64)
+  FF_CASE(true, 64, 256)
+  FF_CASE(true, 64, 128)
+  FF_CASE(true, 64, 64)
+#undef FF_CASE
+  return nullptr;
+}
+
+int validate_chain(const ffChainDesc* ch) {
+  if (!ch) return fail(FF_ERR_ARG, "null chain descriptor");
+  if (ch->kind != FF_KIND_STANDARD && ch->kind != FF_KIND_GATED) return fail(FF_ERR_ARG, "unknown chain kind");
+  if (ch->activation < 0 || ch->activation > FF_ACT_GELU_TANH) return fail(FF_ERR_ARG, "unknown activation");
+  if (ch->element_size != 2) return fail(FF_ERR_UNSUPPORTED, "GPU path executes bf16 storage (element_size 2) only");
+  if (ch->m < 1 || ch->n < 64 || ch->k < 64 || ch->l < 64)
+    return fail(FF_ERR_UNSUPPORTED, "extents below one 64-wide tile");
+  if (ch->k % 64 || ch->n % 64 || ch->l % 64)
+    return fail(FF_ERR_UNSUPPORTED, "n, k, l must be multiples of 64 for the sm_100a kernel");
+  if (ch->m > (1ll << 31) || ch->n > (1ll << 31) || ch->k > (1ll << 31) || ch->l > (1ll << 31))
+    return fail(FF_ERR_UNSUPPORTED, "extent too large");
+  return FF_OK;
+}
+
+// Fill derived fields and check that a physical configuration is executable.
+int finish_config(const ffChainDesc* ch, ffKernelConfig* c) {
+  const bool gated = ch->kind == FF_KIND_GATED;
+  if (c->ring < 1 || c->ring > 16) return fail(FF_ERR_UNSUPPORTED, "ring size must be 1..16");
+  if (c->n_splits < 1) return fail(FF_ERR_UNSUPPORTED, "n_splits must be >= 1");
+  if (!select_kernel(gated, c->nb, c->lb)) return fail(FF_ERR_UNSUPPORTED, "no kernel for (nb, lb)");
+  const int64_t lcover = (int64_t)c->ring * c->lb;
+  if (ch->l % lcover) return fail(FF_ERR_UNSUPPORTED, "ring * lb must divide l");
+  const int64_t nstep = (int64_t)c->n_splits * c->ring * c->nb;
+  if (ch->n % nstep) return fail(FF_ERR_UNSUPPORTED, "n_splits * ring * nb must divide n");
+  c->l_clusters = (int32_t)(ch->l / lcover);
+  c->steps = (int32_t)(ch->n / nstep);
+  c->m_tiles = (int32_t)((ch->m + 127) / 128);
+  const int64_t ctas = (int64_t)c->m_tiles * c->l_clusters * c->n_splits * c->ring;
+  if (ctas > (1ll << 30)) return fail(FF_ERR_UNSUPPORTED, "grid too large");
+  c->grid_ctas = (int32_t)ctas;
+  return FF_OK;
+}
+
+int pick_lb(int64_t cover, int max_ring) {
+  for (int lb : {256, 128, 64})
+    if (cover % lb == 0 && cover / lb <= max_ring) return lb;
+  return 0;
+}
+
+// Grow the number of N splits while the launch underfills the GPU.
+void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
+  for (;;) {
+    const int64_t per = (int64_t)((ch->m + 127) / 128) * (ch->l / ((int64_t)c->ring * c->lb)) * c->ring;
+    const int64_t next = (int64_t)c->n_splits * 2;
+    if (per * next > num_sms) break;
+    if (ch->n % (next * c->ring * c->nb)) break;
+    c->n_splits = (int32_t)next;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ff_last_error(void) { return g_last_error.c_str(); }
+const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
+
+int ff_auto_config(const ffChainDesc* ch, int32_t num_sms, ffKernelConfig* out) {
+  int rc = validate_chain(ch);
+  if (rc) return rc;
+  if (!out) return fail(FF_ERR_ARG, "null output");
+  if (num_sms <= 0) num_sms = 148;
+  ffKernelConfig c = {};
+  const bool gated = ch->kind == FF_KIND_GATED;
+  c.lb = pick_lb(ch->l, 16);
+  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "l cannot be covered by a ring of <= 16 CTAs");
+  c.ring = (int32_t)(ch->l / c.lb);
+  c.nb = gated ? 64 : 128;
+  if (ch->n % ((int64_t)c.ring * c.nb)) c.nb = 64;
+  // a ring must not be larger than the number of C chunks it shares
+  while (c.ring > 1 && ch->n % ((int64_t)c.ring * c.nb)) {
+    if (c.lb < 256 && (ch->l % (c.lb * 2)) == 0) {
+      c.lb *= 2;
+      c.ring = (int32_t)(ch->l / c.lb);
+    } else {
+      break;
+    }
+  }
+  c.n_splits = 1;
+  fill_machine(ch, &c, num_sms);
+  rc = finish_config(ch, &c);
+  if (rc) return rc;
+  *out = c;
+  return FF_OK;
+}
+
+int ff_plan_lower(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out) {
+  int rc = validate_chain(ch);
+  if (rc) return rc;
+  if (!plan || !out) return fail(FF_ERR_ARG, "null plan or output");
+  if (num_sms <= 0) num_sms = 148;
+  const bool gated = ch->kind == FF_KIND_GATED;
+  if (gated && plan->gated_lowering == FF_LOWERING_NA)
+    return fail(FF_ERR_PLAN, "gated chain requires a lowering (spatial_split or doubled_k)");
+  if (!gated && plan->gated_lowering != FF_LOWERING_NA)
+    return fail(FF_ERR_PLAN, "standard chain cannot carry a gated lowering");
+  const int32_t cm = plan->cluster[0], cn = plan->cluster[1], ck = plan->cluster[2], cl = plan->cluster[3];
+  if (cm < 1 || cn < 1 || ck < 1 || cl < 1) return fail(FF_ERR_PLAN, "cluster dims must be positive");
+  if (cl % ck) return fail(FF_ERR_PLAN, "cls_k does not divide cls_l");
+  if ((cn * ck) % cl) return fail(FF_ERR_PLAN, "cls_l does not divide cls_n*cls_k");
+  if ((plan->spatial_mask >> 3) & 1u) return fail(FF_ERR_PLAN, "output-column dimension is grid-spatial");
+  const int64_t ext[4] = {ch->m, ch->n, gated && plan->gated_lowering == FF_LOWERING_DOUBLED_K ? 2 * ch->k : ch->k,
+                          ch->l};
+  for (int d = 0; d < 4; ++d)
+    if (plan->block[d] <= 0 || ext[d] % plan->block[d]) return fail(FF_ERR_PLAN, "block tile does not divide extent");
+
+  // Logical -> physical:
+  //  * the plan's l cover of one cluster (cls_l * blk_l) becomes one shuffle
+  //    ring of CTAs with <= 256 TMEM columns of E each;
+  //  * cls_reduce sets and grid-spatial N clusters become N splits whose E
+  //    partials are reduced across clusters;
+  //  * M trips (any blk_m) become independent 128-row CTAs (M is never reduced);
+  //  * the gated branches (spatial_split or doubled_k) execute as two TMEM
+  //    accumulators of one CTA, combined by the epilogue (all_exchange Mul).
+  ffKernelConfig c = {};
+  const int64_t lcover = (int64_t)cl * plan->block[3];
+  c.lb = pick_lb(lcover, 16);
+  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "plan's l cover cannot be split into <= 16 CTAs of <= 256 columns");
+  c.ring = (int32_t)(lcover / c.lb);
+  const int64_t ncover = (int64_t)cn * plan->block[1];  // cluster n cover (plan.py:236)
+  const int64_t grid_n = ((plan->spatial_mask >> 1) & 1u) ? ch->n / ncover : 1;
+  const int32_t reduce_sets = (cn * ck) / cl;
+  c.n_splits = (int32_t)(grid_n * reduce_sets);
+  c.nb = gated ? 64 : 128;
+  while (c.n_splits > 1 && ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.n_splits /= 2;
+  if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.nb = 64;
+  if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb))
+    return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");
+  fill_machine(ch, &c, num_sms);
+  rc = finish_config(ch, &c);
+  if (rc) return rc;
+  *out = c;
+  return FF_OK;
+}
+
+size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg) {
+  if (!ch || !cfg) return 0;
+  return cfg->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
+}
+
+int ff_chain_kernel_count(const ffChainDesc* ch, const ffKernelConfig* cfg) {
+  if (!ch || !cfg) return 0;
+  return cfg->n_splits > 1 ? 2 : 1;
+}
+
+static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, const ffTensors* t, void* ws,
+                         size_t ws_bytes, void* c_debug, void* stream) {
+  int rc = validate_chain(ch);
+  if (rc) return rc;
+  if (!cfg_in || !t || !t->a || !t->b || !t->d || !t->e) return fail(FF_ERR_ARG, "null tensor pointer");
+  const bool gated = ch->kind == FF_KIND_GATED;
+  if (gated && !t->b1) return fail(FF_ERR_ARG, "gated chain needs B1");
+  for (const void* p : {t->a, t->b, t->d, (const void*)t->e})
+    if (reinterpret_cast<uintptr_t>(p) % 16) return fail(FF_ERR_ARG, "tensors must be 16-byte aligned");
+  ffKernelConfig cfg = *cfg_in;
+  rc = finish_config(ch, &cfg);
+  if (rc) return rc;
+  const size_t need = ff_chain_workspace_bytes(ch, &cfg);
+  if (need && (ws == nullptr || ws_bytes < need)) return fail(FF_ERR_ARG, "workspace too small");
+  LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb);
+  return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int ff_chain_launch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return launch_common(ch, cfg, t, ws, ws_bytes, nullptr, stream);
+}
+
+int ff_chain_launch_debug(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
+                          size_t ws_bytes, void* c_out, void* stream) {
+  return launch_common(ch, cfg, t, ws, ws_bytes, c_out, stream);
+}
+
+int ff_chain_run_plan(const ffChainDesc* ch, const ffPlanDesc* plan, const ffTensors* t, void* ws,
+                      size_t ws_bytes, void* stream) {
+  ffKernelConfig cfg;
+  int rc = ff_plan_lower(ch, plan, num_sms_cached(), &cfg);
+  if (rc) return rc;
+  return launch_common(ch, &cfg, t, ws, ws_bytes, nullptr, stream);
+}
+
+}  // extern "C"
