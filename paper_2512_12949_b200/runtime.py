@@ -1,0 +1,145 @@
+"""GPU runner: ``run(graph, plan, tensors)`` -> E through the C ABI.
+
+Lowering (ff_plan_lower, C++) turns the logical plan into a physical sm_100a
+launch; see DESIGN.md.  Tensors are caller-owned bf16 CUDA tensors in the
+reference layouts A[m,k], B[k,n] / B0,B1[k,n], D[n,l]; the output E[m,l] is
+allocated here unless ``out`` is given.  Work is stream-ordered with no host
+synchronisation.  There is no CPU fallback: a missing library or device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+from . import _native as nat
+from .plan import FusionPlan
+from .workload import DIMS, GATED_FFN, ChainGraph
+
+_workspaces: dict = {}
+
+
+def chain_desc(graph: ChainGraph) -> nat.ChainDesc:
+    d = graph.dims
+    return nat.ChainDesc(nat.KIND[graph.kind], nat.ACT[graph.activation], d.m, d.n, d.k, d.l, 2)
+
+
+def plan_desc(plan: FusionPlan) -> nat.PlanDesc:
+    pd = nat.PlanDesc()
+    pd.spatial_mask = sum(1 << i for i, d in enumerate(DIMS) if d in plan.schedule.spatial)
+    order = plan.schedule.temporal_order
+    for i, d in enumerate(order):
+        pd.temporal[i] = DIMS.index(d)
+    pd.n_temporal = len(order)
+    for i, d in enumerate(DIMS):
+        pd.block[i] = plan.tiles.block[d]
+        pd.cluster[i] = plan.tiles.cluster[d]
+    pd.gated_lowering = nat.LOWERING[plan.gated_lowering]
+    return pd
+
+
+def _num_sms() -> int:
+    import torch
+
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None) -> nat.KernelConfig:
+    """Physical launch configuration for (graph, plan); plan=None lets the
+    runtime choose the hardware-shaped configuration."""
+    lib = nat.load()
+    cfg = nat.KernelConfig()
+    ch = chain_desc(graph)
+    sms = num_sms if num_sms is not None else 148
+    if plan is None:
+        nat.check(lib.ff_auto_config(ctypes.byref(ch), sms, ctypes.byref(cfg)))
+    else:
+        pd = plan_desc(plan)
+        nat.check(lib.ff_plan_lower(ctypes.byref(ch), ctypes.byref(pd), sms, ctypes.byref(cfg)))
+    return cfg
+
+
+def _workspace(nbytes: int, device):
+    import torch
+
+    if nbytes == 0:
+        return None
+    key = (device.index if device.index is not None else torch.cuda.current_device())
+    buf = _workspaces.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _workspaces[key] = buf
+    return buf
+
+
+def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, stream=None, c_debug=None):
+    """Launch one fused chain with an explicit physical configuration."""
+    import torch
+
+    lib = nat.load()
+    if not torch.cuda.is_available():
+        raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
+    gated = graph.kind == GATED_FFN
+    names = ("A", "B0", "B1", "D") if gated else ("A", "B", "D")
+    d = graph.dims
+    shapes = {"A": (d.m, d.k), "B": (d.k, d.n), "B0": (d.k, d.n), "B1": (d.k, d.n), "D": (d.n, d.l)}
+    for name in names:
+        t = tensors[name]
+        if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
+    a = tensors["A"]
+    if out is None:
+        out = torch.empty((d.m, d.l), dtype=torch.bfloat16, device=a.device)
+    ch = chain_desc(graph)
+    ws_bytes = lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(cfg))
+    ws = _workspace(ws_bytes, a.device)
+    tp = nat.Tensors(a.data_ptr(), tensors["B0" if gated else "B"].data_ptr(),
+                     tensors["B1"].data_ptr() if gated else None, tensors["D"].data_ptr(), out.data_ptr())
+    s = stream if stream is not None else torch.cuda.current_stream(a.device)
+    handle = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
+    ws_ptr = ws.data_ptr() if ws is not None else None
+    if c_debug is not None:
+        rc = lib.ff_chain_launch_debug(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(tp), ws_ptr, ws_bytes,
+                                       c_debug.data_ptr(), handle)
+    else:
+        rc = lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(tp), ws_ptr, ws_bytes, handle)
+    nat.check(rc)
+    return out
+
+
+def run(graph: ChainGraph, plan: Optional[FusionPlan], tensors: dict, out=None, stream=None):
+    """Execute the chain under ``plan`` on the current GPU; returns E (bf16)."""
+    return launch(graph, lower(graph, plan, _num_sms()), tensors, out=out, stream=stream)
+
+
+def kernel_launches(graph: ChainGraph, cfg: nat.KernelConfig) -> int:
+    """How many CUDA kernels one launch issues."""
+    lib = nat.load()
+    ch = chain_desc(graph)
+    return int(lib.ff_chain_kernel_count(ctypes.byref(ch), ctypes.byref(cfg)))
+
+
+def profile_best_from_list(graph: ChainGraph, plans, tensors: dict, iters: int = 10, warmup: int = 3):
+    """Alg. 2 line 10 (ProfileBestFromList): time each candidate
+    plan's fused kernel on the device and return [(ms, plan, cfg)] fastest first.
+    Plans with no sm_100a lowering are skipped."""
+    import torch
+
+    timed = []
+    for plan in plans:
+        try:
+            cfg = lower(graph, plan, _num_sms())
+        except nat.UnsupportedPlan:
+            continue
+        out = torch.empty((graph.dims.m, graph.dims.l), dtype=torch.bfloat16, device="cuda")
+        for _ in range(warmup):
+            launch(graph, cfg, tensors, out=out)
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(iters):
+            launch(graph, cfg, tensors, out=out)
+        stop.record()
+        stop.synchronize()
+        timed.append((start.elapsed_time(stop) / iters, plan, cfg))
+    timed.sort(key=lambda x: x[0])
+    return timed
