@@ -1,0 +1,527 @@
+"""Benchmark of the fused GEMM-chain hot path on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload llama1b]
+
+One "step" = one fused chain (GEMM0 -> act/SwiGLU gate -> GEMM1) over one
+batch of M=512 tokens with the weights resident in HBM.  At N>1 (torchrun,
+one rank per GPU) every rank runs its own batch: the token dimension shards
+with no collective on the data path ("scaling": "weak").
+
+Workload (BASELINE.json configs[1]): LLaMA-1B gated SwiGLU FFN, M=512,
+2048 -> 8192 -> 2048, bf16 storage / fp32 accumulation.  The L2 (126 MB) is
+flushed between timed steps (the weights alone are 96 MiB).
+
+JSON keys beyond the base contract: roofline (dominant kernel vs the measured
+bf16 peak), cpu_baseline (the reference CPU path, oracle port, timed on this
+host), e2e (public API with pinned host buffers), cublas_unfused (same config
+through torch.matmul), hbm (algorithmic bytes fused vs unfused), extra (the
+other BASELINE configs, single GPU, same method).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused-chain TFLOP/s & HBM bytes vs unfused cuBLAS, FFN M=512, 1/2/4/8 B200"
+
+# name -> (kind, activation, m, n, k, l, description)
+WORKLOADS = {
+    "llama1b": ("gated_ffn", "silu", 512, 8192, 2048, 2048, "LLaMA-1B gated SwiGLU FFN M=512, 2048->8192->2048"),
+    "gpt67b": ("standard_ffn", "relu", 512, 16384, 4096, 4096, "GPT-6.7B FFN M=512, 4096->16384->4096"),
+    "gpt2s": ("standard_ffn", "gelu", 512, 3072, 768, 768, "GPT-2 small FFN M=512, 768->3072->768, GELU"),
+    "opt13b_m4096": ("standard_ffn", "relu", 4096, 8192, 2048, 2048, "OPT-1.3B FFN M=4096 (per-GPU shard of 32768/8)"),
+}
+DEFAULT_WORKLOAD = "llama1b"
+
+
+def flops_of(kind, m, n, k, l):
+    return 2 * m * k * n * (2 if kind == "gated_ffn" else 1) + 2 * m * n * l
+
+
+def hbm_bytes(kind, m, n, k, l):
+    """Algorithmic bf16 bytes: fused = A + weights + D + E once; unfused adds the C round trip
+    (cuBLAS GEMM -> separate act kernel -> GEMM: C written, act reads+writes, GEMM reads)."""
+    w = k * n * (2 if kind == "gated_ffn" else 1)
+    fused = 2 * (m * k + w + n * l + m * l)
+    c = m * n
+    extra = (2 * c * 2 + c * 3) if kind == "gated_ffn" else 4 * c  # elements moved through HBM
+    return fused, fused + 2 * extra
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return {"bf16_tflops": d.get("bf16_tflops", 1590.0), "hbm_gbs": d.get("hbm_gbs", 6650.0),
+                "source": "measured"}
+    return {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0, "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._pump, daemon=True)
+        self.thread.start()
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc):
+    """One execution of the reference's CPU path for the chain: the plan-faithful
+    tile replay (fuseplan simulate) restated in oracle/ (numpy BLAS, f32)."""
+    import oracle
+
+    return oracle.replay_plan(kind, act, (m, n, k, l), plan_doc, inputs)
+
+
+def cpu_baseline(name, steps=None, budget_s=12.0):
+    """Time the oracle port of the reference CPU path on a bounded sample."""
+    import oracle
+
+    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    plan_doc = _reference_plan(name)
+    rows = m if m <= 512 else 512          # bounded sample: at most 512 token rows
+    inputs = oracle.make_inputs(kind, rows, n, k, l, seed=0, dtype=np.float32)
+    cpu_reference_step(kind, act, rows, n, k, l, inputs, _rows_plan(plan_doc, rows))  # warm-up
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while (steps is None and time.perf_counter() < t_end and len(times) < 20) or (steps is not None and len(times) < steps):
+        t0 = time.perf_counter()
+        cpu_reference_step(kind, act, rows, n, k, l, inputs, _rows_plan(plan_doc, rows))
+        times.append(time.perf_counter() - t0)
+    sec = float(np.median(times))
+    threads = _blas_threads()
+    return {"value": flops_of(kind, rows, n, k, l) / sec / 1e12, "unit": "TFLOP/s", "cores": threads,
+            "kind": "port", "seconds_per_chain": sec, "runs": len(times),
+            "sample": f"{len(times)} plan-faithful replays (oracle.replay_plan, numpy f32 BLAS) of "
+                      f"{kind} m={rows} n={n} k={k} l={l} under the reference top-1 plan (B200 profile)"}
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        if info:
+            return int(max(i.get("num_threads", 1) for i in info))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def _reference_plan(name):
+    """The reference search's top-1 plan for the workload under the B200 profile
+    (committed in paper_2512_12949_b200/plans/plan_cache.json, produced by our bit-exact search)."""
+    from paper_2512_12949_b200 import plan_cache
+
+    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
+    if entry is None:
+        return {"schedule": {"spatial": ["n"], "temporal": ["k", "l", "m"]},
+                "tiles": {"block": {"m": 64, "n": n // 8, "k": k * (2 if kind == "gated_ffn" else 1), "l": l // 4},
+                          "cluster": {"m": 1, "n": 8, "k": 1, "l": 4}},
+                "gated_lowering": "doubled_k" if kind == "gated_ffn" else "n/a"}
+    return entry["top"][0]
+
+
+def _rows_plan(plan_doc, rows):
+    import copy
+
+    p = copy.deepcopy(plan_doc)
+    bm = p["tiles"]["block"]["m"] * p["tiles"]["cluster"]["m"]
+    if rows % bm:
+        p["tiles"]["block"]["m"] = 64
+        p["tiles"]["cluster"]["m"] = 1
+    return p
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def make_device_inputs(kind, m, n, k, l, seed, device):
+    import torch
+
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    def u(*shape):
+        return (torch.rand(*shape, generator=g) * 2 - 1).to(torch.bfloat16).to(device)
+    t = {"A": u(m, k), "D": u(n, l)}
+    if kind == "gated_ffn":
+        t["B0"], t["B1"] = u(k, n), u(k, n)
+    else:
+        t["B"] = u(k, n)
+    return t
+
+
+def graph_of(name):
+    from paper_2512_12949_b200 import workload as W
+
+    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    dims = W.DimensionSpec(m, n, k, l, 2)
+    return W.build_gated_ffn(dims) if kind == "gated_ffn" else W.build_standard_ffn(dims, act)
+
+
+def choose_config(name, tensors):
+    """Plan -> physical launch: top-K reference plans (plan cache) lowered and timed
+    on the device (ProfileBestFromList), plus the runtime's hardware-shaped config."""
+    from paper_2512_12949_b200 import plan_cache, runtime
+    from paper_2512_12949_b200.plan import plan_from_dict
+
+    graph = graph_of(name)
+    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    cands = []
+    entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
+    plans = [plan_from_dict(p) for p in entry["top"]] if entry else []
+    timed = runtime.profile_best_from_list(graph, plans, tensors, iters=5, warmup=2) if plans else []
+    cands += [(ms, cfg, plan.describe()) for ms, plan, cfg in timed]
+    auto = runtime.lower(graph, None)
+    ms_auto = runtime.profile_configs(graph, [auto], tensors, iters=5, warmup=2)[0][0]
+    cands.append((ms_auto, auto, "runtime-auto"))
+    cands.sort(key=lambda c: c[0])
+    return cands[0][1], cands[0][2], [(round(c[0] * 1e3, 2), c[2]) for c in cands]
+
+
+def time_steps(fn, steps, flush, stream):
+    """Per-step CUDA-event times (ms) of fn(), L2 flushed between steps (outside the events)."""
+    import torch
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_12949_b200 import runtime
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    name = args.workload
+    kind, act, m, n, k, l, desc = WORKLOADS[name]
+    graph = graph_of(name)
+    tensors = make_device_inputs(kind, m, n, k, l, seed=1234 + rank, device=dev)
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flush_buf.add_(1.0)
+
+    stream = torch.cuda.current_stream(dev)
+    cfg, cfg_name, candidates = choose_config(name, tensors)
+    out = torch.empty((m, l), dtype=torch.bfloat16, device=dev)
+
+    def step():
+        runtime.launch(graph, cfg, tensors, out=out)
+
+    for _ in range(max(args.warmup, 3)):
+        flush()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    times = time_steps(step, args.steps, flush, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    fl = flops_of(kind, m, n, k, l)
+    value = fl * args.steps * world / (total_ms * 1e-3) / 1e12
+    ms_step = total_ms / args.steps
+
+    # e2e through the public API: pinned host A -> device, chain, E -> pinned host
+    host_a = tensors["A"].cpu().pin_memory()
+    host_e = torch.empty((m, l), dtype=torch.bfloat16).pin_memory()
+    dev_a = torch.empty_like(tensors["A"])
+    e2e_tensors = dict(tensors)
+    e2e_tensors["A"] = dev_a
+
+    def e2e_step():
+        dev_a.copy_(host_a, non_blocking=True)
+        runtime.launch(graph, cfg, e2e_tensors, out=out)
+        host_e.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_times = time_steps(e2e_step, args.steps, flush, stream)
+    e2e_ms = float(sum(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = fl * args.steps * world / (e2e_ms * 1e-3) / 1e12
+
+    # unfused cuBLAS on the same config
+    cub = cublas_unfused(kind, act, tensors, flush, stream, max(args.steps, 5))
+
+    if rank != 0:
+        return None
+    peaks = load_peaks()
+    kern_ms = float(np.median(times))
+    achieved = fl / (kern_ms * 1e-3) / 1e12
+    fused_b, unfused_b = hbm_bytes(kind, m, n, k, l)
+    ncu = load_ncu_summary(name)
+    launches = runtime.kernel_launches(graph, cfg) * args.steps
+    doc = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic U[-1,1] bf16 inputs and weights (seeded)",
+        "config": {"workload": desc, "m_per_gpu": m, "n": n, "k": k, "l": l, "kind": kind, "activation": act,
+                   "global_batch_tokens": m * world, "parallelism": f"token-sharded x{world} (independent per GPU)",
+                   "l2": "flushed between timed steps (256 MiB write)", "launch": cfg.as_dict(),
+                   "plan": cfg_name, "candidates_ms": candidates},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
+                     "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
+                     "traffic": ncu.get("dram_bytes_per_launch"), "peak_source": peaks["source"],
+                     "kernel_ms_median": round(kern_ms, 4)},
+        "e2e": {"value": round(e2e_value, 2), "unit": "TFLOP/s", "h2d_bytes_per_step": int(host_a.numel() * 2),
+                "d2h_bytes_per_step": int(host_e.numel() * 2), "ms_per_step": round(e2e_ms / args.steps, 4),
+                "api": "paper_2512_12949_b200.runtime.launch (C ABI ff_chain_launch)"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "cublas_unfused": cub,
+        "hbm": {"algorithmic_fused_bytes": fused_b, "algorithmic_unfused_bytes": unfused_b,
+                "ncu_fused_dram_bytes": ncu.get("dram_bytes_per_launch"),
+                "ncu_unfused_dram_bytes": ncu.get("cublas_dram_bytes"), "source": ncu.get("source")},
+        "wall_s_timed": round(wall, 3),
+    }
+    return doc
+
+
+def cublas_unfused(kind, act, t, flush, stream, steps):
+    import torch
+
+    f = torch.nn.functional
+    if kind == "gated_ffn":
+        def fn():
+            return (f.silu(t["A"] @ t["B0"]) * (t["A"] @ t["B1"])) @ t["D"]
+    else:
+        actf = {"relu": torch.relu, "silu": f.silu, "gelu": lambda x: f.gelu(x, approximate="tanh"),
+                "identity": lambda x: x}[act]
+
+        def fn():
+            return actf(t["A"] @ t["B"]) @ t["D"]
+    for _ in range(3):
+        fn()
+    times = time_steps(fn, steps, flush, stream)
+    ms = float(np.median(times))
+    m, k = t["A"].shape
+    n, l = t["D"].shape
+    fl = flops_of(kind, m, n, k, l)
+    return {"ms": round(ms, 4), "tflops": round(fl / (ms * 1e-3) / 1e12, 2),
+            "path": "torch.matmul (cuBLAS) + elementwise act, 3-4 kernels"}
+
+
+def load_ncu_summary(name):
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as fh:
+        doc = json.load(fh)
+    entry = doc.get(name, {})
+    entry = dict(entry)
+    entry["source"] = f"profiles/ncu_summary.json ({doc.get('round', '?')})"
+    return entry
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the reference's CPU path (oracle port) on this host, rank 0 only."""
+    if rank != 0:
+        return None
+    kind, act, m, n, k, l, desc = WORKLOADS[args.workload]
+    import oracle
+
+    plan_doc = _rows_plan(_reference_plan(args.workload), m)
+    inputs = oracle.make_inputs(kind, m, n, k, l, seed=0, dtype=np.float32)
+    for _ in range(args.warmup):
+        cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc)
+        times.append(time.perf_counter() - t0)
+    total = float(sum(times))
+    fl = flops_of(kind, m, n, k, l)
+    value = fl * args.steps / total / 1e12
+    cores = _blas_threads()
+    return {
+        "impl": "reference",
+        "metric": METRIC, "value": round(value, 5), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic U[-1,1] f32 (seeded)",
+        "config": {"workload": desc, "m_per_gpu": m, "n": n, "k": k, "l": l, "kind": kind, "activation": act,
+                   "path": "oracle.replay_plan: numpy restatement of fuseplan simulator.execute_plan "
+                           "(the reference's CPU execution path), reference top-1 plan"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.steps} full chains m={m} (one step = one chain)"},
+        "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def run_extra(args):
+    """Other BASELINE configs, single GPU, fused vs cuBLAS (informative)."""
+    import torch
+
+    from paper_2512_12949_b200 import runtime
+
+    out = {}
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush():
+        flush_buf.add_(1.0)
+
+    for name in WORKLOADS:
+        if name == args.workload:
+            continue
+        kind, act, m, n, k, l, desc = WORKLOADS[name]
+        try:
+            graph = graph_of(name)
+            t = make_device_inputs(kind, m, n, k, l, 7, "cuda")
+            cfg, cfg_name, _ = choose_config(name, t)
+            o = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
+            fn = lambda: runtime.launch(graph, cfg, t, out=o)  # noqa: E731
+            for _ in range(3):
+                fn()
+            ms = float(np.median(time_steps(fn, 5, flush, torch.cuda.current_stream())))
+            fl = flops_of(kind, m, n, k, l)
+            out[name] = {"workload": desc, "fused_ms": round(ms, 4), "fused_tflops": round(fl / ms / 1e9, 1),
+                         "launch": cfg.as_dict(), "plan": cfg_name,
+                         "cublas_unfused": cublas_unfused(kind, act, t, flush, torch.cuda.current_stream(), 5)}
+        except Exception as exc:  # informative only
+            out[name] = {"error": repr(exc)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        doc = run_reference(args, rank, world)
+        if doc is not None:
+            print(json.dumps(doc), flush=True)
+        return
+
+    import torch.distributed as dist
+
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    doc = run_ours(args, rank, world, local_rank)
+    if doc is not None:
+        if not args.no_cpu and world == 1:
+            doc["cpu_baseline"] = cpu_baseline(args.workload)
+        if world == 1 and not args.no_extra:
+            doc["extra"] = run_extra(args)
+        print(json.dumps(doc), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

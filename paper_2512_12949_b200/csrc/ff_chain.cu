@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -116,6 +117,8 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
   a.ws = reinterpret_cast<float*>(ws);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
+  a.dbg = 0;
+  if (const char* env = getenv("FF_DEBUG_FLAGS")) a.dbg = atoi(env);
 
   if (cfg->n_splits > 1) {
     cudaError_t e = cudaMemsetAsync(ws, 0, (size_t)M * L * sizeof(float), stream);

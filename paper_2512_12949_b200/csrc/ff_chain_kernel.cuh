@@ -15,17 +15,18 @@
 //     accumulator, double buffered across n-steps), applies the activation /
 //     SwiGLU gate and writes bf16 C into shared memory in the UMMA K-major
 //     128B-swizzled layout (so the tile is directly the A operand of GEMM1);
-//   * dsm_shuffle: the chunks circulate around the ring over distributed
-//     shared memory (cp.async.bulk shared::cta -> shared::cluster with
-//     mbarrier complete_tx, 2 receive buffers, credit barriers between ring
-//     neighbours).  At hop h a CTA multiplies the chunk that originated at
-//     ring member (p-h) mod G with the matching D rows into its E tile;
+//   * dsm_shuffle: every chunk is pushed over distributed shared memory to
+//     the other G-1 ring members (cp.async.bulk shared::cta -> shared::cluster
+//     with mbarrier complete_tx, 2 receive buffers, per-hop credit counters).
+//     At hop h a CTA multiplies the chunk that originated at ring member
+//     (p-h) mod G with the matching D rows into its E tile; the hops of n-step
+//     t are interleaved with the GEMM0 k-blocks of n-step t+1;
 //   * inter-cluster reduce: when N is split across S clusters the E tiles
 //     are combined with red.global.add.v4.f32 into an fp32 workspace, then a
 //     finalize kernel casts to bf16 (simulator.py:371 "+=" into E).
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (+TMEM alloc),
-// w2 DSM ring driver, w3 idle, w4..w7 epilogue (TMEM -> regs -> smem/global).
+// w2 DSM push driver, w3 DSM buffer recycler / credits, w4..w7 epilogue.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -47,6 +48,7 @@ struct ChainArgs {
   __nv_bfloat16* E;    // output (used when S == 1)
   float* ws;           // fp32 accumulation workspace (used when S > 1)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
+  int dbg;                 // debug switches (FF_DEBUG_FLAGS), 0 in production
 };
 
 __device__ __forceinline__ float apply_act(int act, float x) {
@@ -80,7 +82,7 @@ struct ChainCfg {
   static constexpr int kOFF_OWN = kStages * kSTAGE;
   static constexpr int kOFF_RECV = kOFF_OWN + kCHUNK_BYTES;
   static constexpr int kOFF_BAR = kOFF_RECV + 2 * kCHUNK_BYTES;
-  static constexpr int kNUM_BARS = 2 * kStages + 12;
+  static constexpr int kNUM_BARS = 2 * kStages + 13 + 9;  // 13 named barriers + 16 u32 credit counters
   static constexpr int kSMEM = kOFF_BAR + kNUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int kTMEM_E = 2 * kAcc;          // E accumulator column offset
   static constexpr int kTMEM_COLS = 512;
@@ -127,8 +129,9 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t own_full = bx + 32, own_free = bx + 40;
   const uint32_t recv_full[2] = {bx + 48, bx + 56};
   const uint32_t recv_used[2] = {bx + 64, bx + 72};
-  const uint32_t right_free[2] = {bx + 80, bx + 88};
   const uint32_t e_full = bx + 96;
+  auto credit = [&](int h) { return bx + 104 + 4u * h; };  // u32 counters, h = 1..G-1
+  const uint32_t ack_count = credit(0);  // landed-chunk acknowledgements from receivers
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
   const uint32_t own_slot = base + C::kOFF_OWN;
   const uint32_t recv_slot[2] = {base + C::kOFF_RECV, base + C::kOFF_RECV + C::kCHUNK_BYTES};
@@ -143,17 +146,14 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(c_empty[b], 128);
       mbar_init(recv_full[b], 1);
       mbar_init(recv_used[b], 1);
-      mbar_init(right_free[b], 1);
     }
+    for (int h = 0; h < 16; ++h) *reinterpret_cast<volatile uint32_t*>(smem_gen + (credit(h) - base)) = 0u;
     mbar_init(own_full, 128);
     mbar_init(own_free, G > 1 ? 2 : 1);
     mbar_init(e_full, 1);
     fence_mbar_init();
-    // receive buffers armed for their first use; right neighbour's buffers start free
-    for (int b = 0; b < 2; ++b) {
-      mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
-      mbar_arrive(right_free[b]);
-    }
+    // receive buffers armed for their first use
+    for (int b = 0; b < 2; ++b) mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
   }
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
@@ -178,9 +178,11 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
-      auto load_gemm0 = [&](int t) {
+      // Loads follow the MMA issue order exactly: GEMM0(t+1) k-blocks are
+      // interleaved with GEMM1(t) ring hops (slot h = k-blocks [h*KB/G, (h+1)*KB/G)).
+      auto load_gemm0 = [&](int t, int kb0, int kb1) {
         const int n0 = n_split0 + (t * G + (int)p) * kNB;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);
@@ -196,25 +198,27 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
       };
-      auto load_gemm1 = [&](int t) {
-        for (int h = 0; h < G; ++h) {
-          const int origin = ((int)p - h + G) % G;
-          const int nrow0 = n_split0 + (t * G + origin) * kNB;
-          for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-            mbar_wait(empty_bar(stage), phase ^ 1);
-            const uint32_t sb = base + stage * C::kSTAGE;
-            mbar_expect_tx(full_bar(stage), C::kD_BYTES);
+      auto load_hop = [&](int t, int h) {
+        const int origin = ((int)p - h + G) % G;
+        const int nrow0 = n_split0 + (t * G + origin) * kNB;
+        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sb = base + stage * C::kSTAGE;
+          mbar_expect_tx(full_bar(stage), C::kD_BYTES);
 #pragma unroll
-            for (int j = 0; j < kLB / 64; ++j)
-              tma_load_2d(sb + j * 8192, &tmD, full_bar(stage), l0 + 64 * j, nrow0 + kb2 * C::BK);
-            next();
-          }
+          for (int j = 0; j < kLB / 64; ++j)
+            tma_load_2d(sb + j * 8192, &tmD, full_bar(stage), l0 + 64 * j, nrow0 + kb2 * C::BK);
+          next();
         }
       };
-      load_gemm0(0);
+      load_gemm0(0, 0, kblocks);
       for (int t = 0; t < steps; ++t) {
-        if (t + 1 < steps) load_gemm0(t + 1);
-        load_gemm1(t);
+        for (int h = 0; h < G; ++h) {
+          const int s0 = (args.dbg & 8) ? (h ? kblocks : 0) : h * kblocks / G;
+          const int s1 = (args.dbg & 8) ? kblocks : (h + 1) * kblocks / G;
+          if (t + 1 < steps) load_gemm0(t + 1, s0, s1);
+          load_hop(t, h);
+        }
       }
     }
   } else if (warp == 1) {
@@ -229,13 +233,14 @@ __global__ void __launch_bounds__(256, 1)
       };
       constexpr uint32_t idesc0 = idesc_bf16(128, kNB, 0, 1);
       constexpr uint32_t idesc1 = idesc_bf16(128, kLB, 0, 1);
-      auto gemm0 = [&](int t) {
+      auto gemm0 = [&](int t, int kb0, int kb1) {
         const int cb = t & 1;
-        const int use = t >> 1;
-        mbar_wait(c_empty[cb], (use & 1) ^ 1);
-        tc_fence_after();
+        if (kb0 == 0) {
+          mbar_wait(c_empty[cb], ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
         const uint32_t tacc = tmem_base + cb * C::kAcc;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
@@ -256,84 +261,102 @@ __global__ void __launch_bounds__(256, 1)
           umma_commit(empty_bar(stage));
           next();
         }
-        umma_commit(c_full[cb]);
+        if (kb1 == kblocks) umma_commit(c_full[cb]);
       };
       int ri = 0;
       bool e_started = false;
-      auto gemm1 = [&](int t) {
-        for (int h = 0; h < G; ++h) {
-          uint32_t slot;
-          int b = 0;
-          if (h == 0) {
-            mbar_wait(own_full, t & 1);
-            slot = own_slot;
-          } else {
-            b = ri & 1;
-            mbar_wait_cluster(recv_full[b], (ri >> 1) & 1);
-            slot = recv_slot[b];
-          }
+      auto hop = [&](int t, int h) {
+        uint32_t slot;
+        int b = 0;
+        if (h == 0) {
+          mbar_wait(own_full, t & 1);
+          slot = own_slot;
+        } else {
+          b = ri & 1;
+          mbar_wait_cluster(recv_full[b], (ri >> 1) & 1);
+          slot = recv_slot[b];
+        }
+        tc_fence_after();
+        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+          mbar_wait(full_bar(stage), phase);
           tc_fence_after();
-          for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-            mbar_wait(full_bar(stage), phase);
-            tc_fence_after();
-            const uint32_t sb = base + stage * C::kSTAGE;
-            const uint32_t ab = slot + kb2 * (C::BM * C::BK * 2);
+          const uint32_t sb = base + stage * C::kSTAGE;
+          const uint32_t ab = slot + kb2 * (C::BM * C::BK * 2);
 #pragma unroll
-            for (int kk = 0; kk < C::BK / 16; ++kk) {
-              const uint64_t ad = desc_kmajor_sw128(ab + kk * 32);
-              const uint64_t bd = desc_mnmajor_sw128(sb + kk * 2048, 8192);
-              umma_bf16(tmem_base + C::kTMEM_E, ad, bd, idesc1, e_started ? 1u : 0u);
-              e_started = true;
-            }
-            umma_commit(empty_bar(stage));
-            next();
+          for (int kk = 0; kk < C::BK / 16; ++kk) {
+            const uint64_t ad = desc_kmajor_sw128(ab + kk * 32);
+            const uint64_t bd = desc_mnmajor_sw128(sb + kk * 2048, 8192);
+            umma_bf16(tmem_base + C::kTMEM_E, ad, bd, idesc1, e_started ? 1u : 0u);
+            e_started = true;
           }
-          if (h == 0) {
-            umma_commit(own_free);
-          } else {
-            umma_commit(recv_used[b]);
-            ++ri;
-          }
+          umma_commit(empty_bar(stage));
+          next();
+        }
+        if (h == 0) {
+          umma_commit(own_free);
+        } else {
+          umma_commit(recv_used[b]);
+          ++ri;
         }
       };
-      gemm0(0);
+      gemm0(0, 0, kblocks);
       for (int t = 0; t < steps; ++t) {
-        if (t + 1 < steps) gemm0(t + 1);
-        gemm1(t);
+        for (int h = 0; h < G; ++h) {
+          const int s0 = (args.dbg & 8) ? (h ? kblocks : 0) : h * kblocks / G;
+          const int s1 = (args.dbg & 8) ? kblocks : (h + 1) * kblocks / G;
+          if (t + 1 < steps) gemm0(t + 1, s0, s1);
+          hop(t, h);
+        }
       }
       umma_commit(e_full);
     }
   } else if (warp == 2) {
-    // ===================== DSM ring driver (dsm_shuffle) =====================
+    // ============ dsm_shuffle, send side: direct pushes of the own chunk ============
+    // At hop h ring member q consumes the chunk of origin (q-h) mod G, so origin
+    // p pushes its chunk to (p+h) mod G in hop order; no store-and-forward chain.
+    // Receiver q's global receive index R = t*(G-1) + h-1 selects buffer R & 1;
+    // reusing a buffer needs a credit (remote increment of counter h) sent by
+    // the receiver once it consumed receive R-2.
     if (G > 1 && elect_one()) {
-      const uint32_t right = (p + 1) % G;
-      const uint32_t left = (p + G - 1) % G;
-      int sent = 0, ri = 0;
-      auto push = [&](uint32_t src) {
-        const int b = sent & 1;
-        mbar_wait(right_free[b], (sent >> 1) & 1);
-        dsm_bulk_push(mapa(recv_slot[b], right), src, C::kCHUNK_BYTES, mapa(recv_full[b], right));
-        bulk_commit();
-        ++sent;
-      };
       for (int t = 0; t < steps; ++t) {
         mbar_wait(own_full, t & 1);
-        push(own_slot);
-        bulk_wait_read0();
-        mbar_arrive(own_free);
         for (int h = 1; h < G; ++h) {
-          const int b = ri & 1;
-          const uint32_t ph = (ri >> 1) & 1;
-          mbar_wait_cluster(recv_full[b], ph);
-          if (h + 1 < G) {
-            push(recv_slot[b]);
-            bulk_wait_read0();
+          const uint32_t dest = (p + h) % G;
+          const int R = t * (G - 1) + h - 1;
+          if (R >= 2) {
+            // credits on counter h arrive once per step from step `first` on
+            const int first = (3 - h) <= 0 ? 0 : (3 - h + G - 2) / (G - 1);
+            credit_wait(credit(h), (uint32_t)(t - first + 1));
           }
-          mbar_wait(recv_used[b], ph);
-          // buffer b is free again: arm it for its next use and credit the left neighbour
+          if (args.dbg & 2) asm volatile("fence.proxy.async;" ::: "memory");
+          const int b = R & 1;
+          dsm_bulk_push(mapa(recv_slot[b], dest), own_slot, C::kCHUNK_BYTES, mapa(recv_full[b], dest));
+        }
+        // A shared::cta -> shared::cluster bulk copy completes only through the
+        // destination's mbarrier (it is not a bulk-group op), so the own slot is
+        // free once every receiver acknowledged that its copy landed.
+        credit_wait(ack_count, (uint32_t)((t + 1) * (G - 1)));
+        mbar_arrive(own_free);
+      }
+    }
+  } else if (warp == 3) {
+    // ============ dsm_shuffle, receive side: recycle buffers, credit the next writer ============
+    if (G > 1 && elect_one()) {
+      const int total = steps * (G - 1);
+      for (int R = 0; R < total; ++R) {
+        const int b = R & 1;
+        const uint32_t ph = (R >> 1) & 1;
+        // landed: acknowledge to the origin so it may overwrite its own slot
+        mbar_wait_cluster(recv_full[b], ph);
+        const int h = R % (G - 1) + 1;
+        credit_add_remote(mapa(ack_count, (p + G - h) % G));
+        // consumed: re-arm the buffer and credit the writer of receive R+2
+        mbar_wait(recv_used[b], ph);
+        if (R + 2 < total) {
           mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
-          mbar_arrive_remote(mapa(right_free[b], left));
-          ++ri;
+          const int hn = (R + 2) % (G - 1) + 1;
+          const uint32_t writer = (p + G - hn) % G;
+          credit_add_remote(mapa(credit(hn), writer));
         }
       }
     }
@@ -347,6 +370,11 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(c_full[cb], (t >> 1) & 1);
       tc_fence_after();
       mbar_wait(own_free, (t & 1) ^ 1);
+      if (args.dbg & 4) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < 40000) {
+        }
+      }
       const uint32_t tacc = lane_base + cb * C::kAcc;
 #pragma unroll 1
       for (int c0 = 0; c0 < C::kCW; c0 += 16) {

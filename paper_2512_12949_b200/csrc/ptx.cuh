@@ -102,12 +102,40 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
       : "memory");
   return ok != 0;
 }
+// Watchdog: a wait that never completes is a protocol bug; trap (the launch then
+// fails with an error) instead of hanging the GPU.  try_wait suspends for a
+// hardware-chosen interval per call, so 2^26 polls is several seconds.
+#ifndef FF_WATCHDOG_POLLS
+#define FF_WATCHDOG_POLLS (1u << 26)
+#endif
+__device__ __forceinline__ void watchdog_trap() { asm volatile("trap;"); }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
   }
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t polls = 0;
   while (!mbar_try_wait_cluster(bar, parity)) {
+    if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+  }
+}
+
+// Monotonic credit counters in shared memory (no phase aliasing, unlike an
+// mbarrier that can be completed twice before the waiter looks).
+__device__ __forceinline__ void credit_add_remote(uint32_t cluster_addr) {
+  asm volatile("red.release.cluster.shared::cluster.add.u32 [%0], 1;" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void credit_wait(uint32_t addr, uint32_t target) {
+  uint32_t polls = 0;
+  while ((int)(ld_acquire_cluster_u32(addr) - target) < 0) {
+    if (++polls == 16 * FF_WATCHDOG_POLLS) watchdog_trap();
   }
 }
 

@@ -143,3 +143,22 @@ def profile_best_from_list(graph: ChainGraph, plans, tensors: dict, iters: int =
         timed.append((start.elapsed_time(stop) / iters, plan, cfg))
     timed.sort(key=lambda x: x[0])
     return timed
+
+
+def profile_configs(graph: ChainGraph, cfgs, tensors: dict, iters: int = 10, warmup: int = 3):
+    """Time explicit physical configurations; returns [(ms, cfg)] in input order."""
+    import torch
+
+    out = []
+    res = torch.empty((graph.dims.m, graph.dims.l), dtype=torch.bfloat16, device="cuda")
+    for cfg in cfgs:
+        for _ in range(warmup):
+            launch(graph, cfg, tensors, out=res)
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(iters):
+            launch(graph, cfg, tensors, out=res)
+        stop.record()
+        stop.synchronize()
+        out.append((start.elapsed_time(stop) / iters, cfg))
+    return out
