@@ -71,16 +71,23 @@ typedef struct ffPlanDesc {
   int32_t gated_lowering;  /* FF_LOWERING_* */
 } ffPlanDesc;
 
+/* Shuffle transport of the intermediate C between ring members. */
+#define FF_XCHG_DSM 0 /* distributed shared memory pushes inside a thread-block cluster */
+#define FF_XCHG_L2 1  /* TMA store / TMA load through an L2-resident scratch (cooperative launch) */
+
 /* Physical launch configuration produced by the lowering. */
 typedef struct ffKernelConfig {
-  int32_t ring;        /* CTAs per cluster in the shuffle ring (cls_shuffle) */
-  int32_t n_splits;    /* clusters splitting N (inter-cluster reduce when > 1) */
+  int32_t ring;        /* CTAs sharing one C tile (cls_shuffle of the plan) */
+  int32_t n_splits;    /* N splits whose E partials are reduced across rings (inter-cluster reduce) */
   int32_t nb;          /* C chunk width per CTA per n-step (columns) */
   int32_t lb;          /* E columns owned by one CTA (TMEM accumulator width) */
-  int32_t m_tiles;     /* ceil(m / 128) */
-  int32_t l_clusters;  /* l / (ring * lb) */
-  int32_t steps;       /* n-steps per split */
-  int32_t grid_ctas;   /* total CTAs launched */
+  int32_t exchange;    /* FF_XCHG_DSM | FF_XCHG_L2 */
+  int32_t m_tiles;     /* derived: ceil(m / 128) */
+  int32_t l_clusters;  /* derived: l / (ring * lb) */
+  int32_t steps;       /* derived: n-steps per split */
+  int32_t units;       /* derived: m_tiles * l_clusters * n_splits work units */
+  int32_t rings;       /* derived: co-resident rings launched (persistent over units) */
+  int32_t grid_ctas;   /* derived: rings * ring */
 } ffKernelConfig;
 
 /* Tensors: row-major, the reference layouts (simulator.py:112-123):
@@ -93,13 +100,23 @@ typedef struct ffTensors {
   void* e;
 } ffTensors;
 
-/* Lower a reference plan to a physical launch (no GPU work). */
+/* Lower a reference plan to a physical launch (no GPU work).  The plan's
+ * cls_shuffle ring becomes one thread-block cluster exchanging C over DSM. */
 int ff_plan_lower(const ffChainDesc* chain, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out);
 
-/* Choose the physical launch for a chain without a reference plan. */
+/* Same, with an explicit shuffle transport (FF_XCHG_DSM | FF_XCHG_L2). */
+int ff_plan_lower_ex(const ffChainDesc* chain, const ffPlanDesc* plan, int32_t num_sms, int32_t exchange,
+                     ffKernelConfig* out);
+
+/* Choose the physical launch for a chain without a reference plan (L2 transport). */
 int ff_auto_config(const ffChainDesc* chain, int32_t num_sms, ffKernelConfig* out);
 
-/* Workspace (device bytes) the launch needs; 0 when none. */
+/* Same, with an explicit shuffle transport. */
+int ff_auto_config_ex(const ffChainDesc* chain, int32_t num_sms, int32_t exchange, ffKernelConfig* out);
+
+/* Workspace (device bytes) the launch needs; 0 when none.  The workspace must be
+ * zero-filled once when first allocated; it never needs clearing again (the L2
+ * transport's ready flags are epoch-stamped). */
 size_t ff_chain_workspace_bytes(const ffChainDesc* chain, const ffKernelConfig* cfg);
 
 /* Execute the fused chain with an explicit physical configuration.

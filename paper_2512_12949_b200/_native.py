@@ -26,11 +26,14 @@ FF_ERR_ARG = 5
 KIND = {"standard_ffn": 0, "gated_ffn": 1}
 ACT = {"identity": 0, "relu": 1, "silu": 2, "gelu": 3}
 LOWERING = {"n/a": 0, "spatial_split": 1, "doubled_k": 2}
+XCHG_DSM, XCHG_L2 = 0, 1
 
 # Exported symbols (must match include/ff_chain.h).
 EXPORTS = (
     "ff_plan_lower",
+    "ff_plan_lower_ex",
     "ff_auto_config",
+    "ff_auto_config_ex",
     "ff_chain_workspace_bytes",
     "ff_chain_launch",
     "ff_chain_run_plan",
@@ -82,9 +85,12 @@ class KernelConfig(ctypes.Structure):
         ("n_splits", ctypes.c_int32),
         ("nb", ctypes.c_int32),
         ("lb", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
         ("m_tiles", ctypes.c_int32),
         ("l_clusters", ctypes.c_int32),
         ("steps", ctypes.c_int32),
+        ("units", ctypes.c_int32),
+        ("rings", ctypes.c_int32),
         ("grid_ctas", ctypes.c_int32),
     ]
 
@@ -120,6 +126,8 @@ def load(path: str = LIB_PATH):
         P = ctypes.POINTER
         lib.ff_plan_lower.argtypes = [P(ChainDesc), P(PlanDesc), ctypes.c_int32, P(KernelConfig)]
         lib.ff_auto_config.argtypes = [P(ChainDesc), ctypes.c_int32, P(KernelConfig)]
+        lib.ff_plan_lower_ex.argtypes = [P(ChainDesc), P(PlanDesc), ctypes.c_int32, ctypes.c_int32, P(KernelConfig)]
+        lib.ff_auto_config_ex.argtypes = [P(ChainDesc), ctypes.c_int32, ctypes.c_int32, P(KernelConfig)]
         lib.ff_chain_workspace_bytes.argtypes = [P(ChainDesc), P(KernelConfig)]
         lib.ff_chain_workspace_bytes.restype = ctypes.c_size_t
         lib.ff_chain_launch.argtypes = [P(ChainDesc), P(KernelConfig), P(Tensors), ctypes.c_void_p,

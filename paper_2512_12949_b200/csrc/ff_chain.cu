@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -69,39 +71,109 @@ int num_sms_cached() {
 // ---------------------------------------------------------------------------
 // kernel table
 // ---------------------------------------------------------------------------
-template <bool kGated, int kNB, int kLB>
+template <bool kGated, int kNB, int kLB, int kMode>
 struct StagesFor {
   static constexpr int kBudget = 232448;
-  using Probe = ff::ChainCfg<kGated, kNB, kLB, 1>;
+  using Probe = ff::ChainCfg<kGated, kNB, kLB, 1, kMode>;
   static constexpr int kFixed = Probe::kSMEM - Probe::kSTAGE - 2 * 8;  // everything but the stages
   static constexpr int kMax = (kBudget - kFixed - 64) / (Probe::kSTAGE + 16);
   static constexpr int value = kMax > 6 ? 6 : kMax;
 };
 
-template <bool kGated, int kNB, int kLB>
+// Co-resident clusters of a given size on a 148-SM B200 with ~225 KB smem per
+// CTA (cudaOccupancyMaxActiveClusters, profiles/r01/dsm_bandwidth.log).
+int table_active_clusters(int cluster, int num_sms) {
+  int n;
+  switch (cluster) {
+    case 1: n = 148; break;
+    case 2: n = 74; break;
+    case 4: n = 33; break;
+    case 8: n = 15; break;
+    case 16: n = 7; break;
+    default: n = (148 / cluster) * 3 / 4; break;
+  }
+  return num_sms >= 148 ? n : (n * num_sms) / 148 > 0 ? (n * num_sms) / 148 : 1;
+}
+
+struct WsLayout {
+  size_t e_off, c_off, f_off, total;
+};
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
+  WsLayout w{};
+  size_t off = 0;
+  w.e_off = off;
+  if (c->n_splits > 1) off = align256(off + (size_t)ch->m * ch->l * sizeof(float));
+  w.c_off = off;
+  if (c->exchange == FF_XCHG_L2 && c->ring > 1) {
+    off = align256(off + (size_t)c->m_tiles * 128 * ch->n * 2);
+  }
+  w.f_off = off;
+  if (c->exchange == FF_XCHG_L2) off = align256(off + (size_t)c->units * c->steps * c->ring * sizeof(uint32_t));
+  w.total = off;
+  return w;
+}
+
+std::atomic<uint32_t> g_epoch{0};
+
+template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
                 void* c_debug, cudaStream_t stream) {
-  constexpr int kStages = StagesFor<kGated, kNB, kLB>::value;
+  constexpr int kStages = StagesFor<kGated, kNB, kLB, kMode>::value;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
-  using C = ff::ChainCfg<kGated, kNB, kLB, kStages>;
-  auto kern = ff::ff_chain_kernel<kGated, kNB, kLB, kStages>;
+  using C = ff::ChainCfg<kGated, kNB, kLB, kStages, kMode>;
+  auto kern = ff::ff_chain_kernel<kGated, kNB, kLB, kStages, kMode>;
 
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM);
-    if (attr_err == cudaSuccess)
+    if (attr_err == cudaSuccess && kMode == ff::XCHG_DSM)
       attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
-  if (attr_err != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+  if (attr_err != cudaSuccess)
+    return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
-  CUtensorMap mA, mB0, mB1, mD;
   const uint64_t M = ch->m, N = ch->n, K = ch->k, L = ch->l;
+  const WsLayout wl = ws_layout(ch, cfg);
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  CUtensorMap mA, mB0, mB1, mD, mC;
   bool ok = make_map(&mA, t->a, M, K, 64, 128);
   ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
   ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
   ok = ok && make_map(&mD, t->d, N, L, 64, 64);
+  const bool l2x = (kMode == ff::XCHG_L2 && cfg->ring > 1);
+  ok = ok && make_map(&mC, l2x ? (const void*)(wsb + wl.c_off) : t->a, l2x ? (uint64_t)cfg->m_tiles * 128 : M,
+                      l2x ? N : K, 64, 128);
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+
+  cudaLaunchConfig_t lc = {};
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = C::kSMEM;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  int rings;
+  if (kMode == ff::XCHG_DSM) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cfg->ring;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3(cfg->ring, 1, 1);
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0)
+      active = table_active_clusters(cfg->ring, num_sms_cached());
+    rings = std::min(cfg->units, active);
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    rings = std::min(cfg->units, num_sms_cached() / cfg->ring);
+    if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring larger than the number of SMs");
+  }
+  lc.gridDim = dim3(rings * cfg->ring, 1, 1);
 
   ff::ChainArgs a;
   a.M = (int)M;
@@ -113,37 +185,25 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.steps = cfg->steps;
   a.m_tiles = cfg->m_tiles;
   a.l_clusters = cfg->l_clusters;
+  a.n_units = cfg->units;
+  a.n_rings = rings;
   a.act = ch->activation;
+  a.epoch = g_epoch.fetch_add(1) + 1;
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
-  a.ws = reinterpret_cast<float*>(ws);
+  a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
+  a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
-  a.dbg = 0;
-  if (const char* env = getenv("FF_DEBUG_FLAGS")) a.dbg = atoi(env);
 
   if (cfg->n_splits > 1) {
-    cudaError_t e = cudaMemsetAsync(ws, 0, (size_t)M * L * sizeof(float), stream);
+    cudaError_t e = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e));
   }
-
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(cfg->grid_ctas, 1, 1);
-  lc.blockDim = dim3(256, 1, 1);
-  lc.dynamicSmemBytes = C::kSMEM;
-  lc.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cfg->ring;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  lc.attrs = attr;
-  lc.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, a);
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
   if (cfg->n_splits > 1) {
     const size_t n = (size_t)M * L;
-    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(reinterpret_cast<const float*>(ws),
-                                                                      a.E, n);
+    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(a.ws, a.E, n);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
   }
@@ -152,9 +212,11 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
 
 using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);
 
-LaunchFn select_kernel(bool gated, int nb, int lb) {
-#define FF_CASE(G, NB, LB) \
-  if (gated == G && nb == NB && lb == LB) return &launch_impl<G, NB, LB>;
+LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
+#define FF_CASE(G, NB, LB)                                                    \
+  if (gated == G && nb == NB && lb == LB)                                     \
+    return mode == FF_XCHG_DSM ? &launch_impl<G, NB, LB, ff::XCHG_DSM>        \
+                               : &launch_impl<G, NB, LB, ff::XCHG_L2>;
   FF_CASE(false, 128, 256)
   FF_CASE(false, 128, 128)
   FF_CASE(false, 128, 64)
@@ -183,11 +245,13 @@ int validate_chain(const ffChainDesc* ch) {
 }
 
 // Fill derived fields and check that a physical configuration is executable.
-int finish_config(const ffChainDesc* ch, ffKernelConfig* c) {
+int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const bool gated = ch->kind == FF_KIND_GATED;
-  if (c->ring < 1 || c->ring > 16) return fail(FF_ERR_UNSUPPORTED, "ring size must be 1..16");
+  if (c->exchange != FF_XCHG_DSM && c->exchange != FF_XCHG_L2) return fail(FF_ERR_ARG, "unknown exchange");
+  if (c->ring < 1 || c->ring > (c->exchange == FF_XCHG_DSM ? 16 : num_sms))
+    return fail(FF_ERR_UNSUPPORTED, "ring size out of range (DSM rings are clusters of <= 16 CTAs)");
   if (c->n_splits < 1) return fail(FF_ERR_UNSUPPORTED, "n_splits must be >= 1");
-  if (!select_kernel(gated, c->nb, c->lb)) return fail(FF_ERR_UNSUPPORTED, "no kernel for (nb, lb)");
+  if (!select_kernel(gated, c->nb, c->lb, c->exchange)) return fail(FF_ERR_UNSUPPORTED, "no kernel for (nb, lb)");
   const int64_t lcover = (int64_t)c->ring * c->lb;
   if (ch->l % lcover) return fail(FF_ERR_UNSUPPORTED, "ring * lb must divide l");
   const int64_t nstep = (int64_t)c->n_splits * c->ring * c->nb;
@@ -195,9 +259,12 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c) {
   c->l_clusters = (int32_t)(ch->l / lcover);
   c->steps = (int32_t)(ch->n / nstep);
   c->m_tiles = (int32_t)((ch->m + 127) / 128);
-  const int64_t ctas = (int64_t)c->m_tiles * c->l_clusters * c->n_splits * c->ring;
-  if (ctas > (1ll << 30)) return fail(FF_ERR_UNSUPPORTED, "grid too large");
-  c->grid_ctas = (int32_t)ctas;
+  const int64_t units = (int64_t)c->m_tiles * c->l_clusters * c->n_splits;
+  if (units > (1ll << 30)) return fail(FF_ERR_UNSUPPORTED, "grid too large");
+  c->units = (int32_t)units;
+  const int64_t max_rings = c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / c->ring;
+  c->rings = (int32_t)std::min<int64_t>(units, max_rings);
+  c->grid_ctas = c->rings * c->ring;
   return FF_OK;
 }
 
@@ -207,12 +274,13 @@ int pick_lb(int64_t cover, int max_ring) {
   return 0;
 }
 
-// Grow the number of N splits while the launch underfills the GPU.
+// Grow the number of N splits while the units do not yet fill the co-resident rings.
 void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
+  const int max_rings = c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / c->ring;
   for (;;) {
-    const int64_t per = (int64_t)((ch->m + 127) / 128) * (ch->l / ((int64_t)c->ring * c->lb)) * c->ring;
+    const int64_t per = (int64_t)((ch->m + 127) / 128) * (ch->l / ((int64_t)c->ring * c->lb));
     const int64_t next = (int64_t)c->n_splits * 2;
-    if (per * next > num_sms) break;
+    if (per * next > max_rings) break;
     if (ch->n % (next * c->ring * c->nb)) break;
     c->n_splits = (int32_t)next;
   }
@@ -225,36 +293,34 @@ extern "C" {
 const char* ff_last_error(void) { return g_last_error.c_str(); }
 const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
 
-int ff_auto_config(const ffChainDesc* ch, int32_t num_sms, ffKernelConfig* out) {
+int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {
   int rc = validate_chain(ch);
   if (rc) return rc;
   if (!out) return fail(FF_ERR_ARG, "null output");
   if (num_sms <= 0) num_sms = 148;
   ffKernelConfig c = {};
+  c.exchange = exchange;
   const bool gated = ch->kind == FF_KIND_GATED;
-  c.lb = pick_lb(ch->l, 16);
-  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "l cannot be covered by a ring of <= 16 CTAs");
+  const int max_ring = exchange == FF_XCHG_DSM ? 16 : num_sms;
+  c.lb = pick_lb(ch->l, max_ring);
+  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "l cannot be covered by one ring");
   c.ring = (int32_t)(ch->l / c.lb);
   c.nb = gated ? 64 : 128;
   if (ch->n % ((int64_t)c.ring * c.nb)) c.nb = 64;
-  // a ring must not be larger than the number of C chunks it shares
-  while (c.ring > 1 && ch->n % ((int64_t)c.ring * c.nb)) {
-    if (c.lb < 256 && (ch->l % (c.lb * 2)) == 0) {
-      c.lb *= 2;
-      c.ring = (int32_t)(ch->l / c.lb);
-    } else {
-      break;
-    }
-  }
   c.n_splits = 1;
   fill_machine(ch, &c, num_sms);
-  rc = finish_config(ch, &c);
+  rc = finish_config(ch, &c, num_sms);
   if (rc) return rc;
   *out = c;
   return FF_OK;
 }
 
-int ff_plan_lower(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out) {
+int ff_auto_config(const ffChainDesc* ch, int32_t num_sms, ffKernelConfig* out) {
+  return ff_auto_config_ex(ch, num_sms, FF_XCHG_L2, out);
+}
+
+int ff_plan_lower_ex(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms, int32_t exchange,
+                     ffKernelConfig* out) {
   int rc = validate_chain(ch);
   if (rc) return rc;
   if (!plan || !out) return fail(FF_ERR_ARG, "null plan or output");
@@ -274,18 +340,20 @@ int ff_plan_lower(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms
   for (int d = 0; d < 4; ++d)
     if (plan->block[d] <= 0 || ext[d] % plan->block[d]) return fail(FF_ERR_PLAN, "block tile does not divide extent");
 
-  // Logical -> physical (see DESIGN.md "lowering"):
+  // Logical -> physical (DESIGN.md "Lowering"):
   //  * the plan's l cover of one cluster (cls_l * blk_l) becomes one shuffle
-  //    ring of CTAs with <= 256 TMEM columns of E each;
+  //    ring of CTAs holding <= 256 TMEM columns of E each;
   //  * cls_reduce sets and grid-spatial N clusters become N splits whose E
-  //    partials are reduced across clusters;
-  //  * M trips (any blk_m) become independent 128-row CTAs (M is never reduced);
+  //    partials are reduced across rings (inter-cluster reduce);
+  //  * M trips (any blk_m) become independent 128-row work units (M is never
+  //    reduced), distributed over co-resident rings;
   //  * the gated branches (spatial_split or doubled_k) execute as two TMEM
   //    accumulators of one CTA, combined by the epilogue (all_exchange Mul).
   ffKernelConfig c = {};
+  c.exchange = exchange;
   const int64_t lcover = (int64_t)cl * plan->block[3];
-  c.lb = pick_lb(lcover, 16);
-  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "plan's l cover cannot be split into <= 16 CTAs of <= 256 columns");
+  c.lb = pick_lb(lcover, exchange == FF_XCHG_DSM ? 16 : num_sms);
+  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "plan's l cover cannot be split into ring members of <= 256 columns");
   c.ring = (int32_t)(lcover / c.lb);
   const int64_t ncover = (int64_t)cn * plan->block[1];  // cluster n cover (plan.py:236)
   const int64_t grid_n = ((plan->spatial_mask >> 1) & 1u) ? ch->n / ncover : 1;
@@ -297,15 +365,21 @@ int ff_plan_lower(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms
   if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb))
     return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");
   fill_machine(ch, &c, num_sms);
-  rc = finish_config(ch, &c);
+  rc = finish_config(ch, &c, num_sms);
   if (rc) return rc;
   *out = c;
   return FF_OK;
 }
 
-size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg) {
-  if (!ch || !cfg) return 0;
-  return cfg->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
+int ff_plan_lower(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out) {
+  return ff_plan_lower_ex(ch, plan, num_sms, FF_XCHG_DSM, out);
+}
+
+size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg_in) {
+  if (!ch || !cfg_in) return 0;
+  ffKernelConfig cfg = *cfg_in;
+  if (finish_config(ch, &cfg, 148)) return 0;
+  return ws_layout(ch, &cfg).total;
 }
 
 int ff_chain_kernel_count(const ffChainDesc* ch, const ffKernelConfig* cfg) {
@@ -323,11 +397,12 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   for (const void* p : {t->a, t->b, t->d, (const void*)t->e})
     if (reinterpret_cast<uintptr_t>(p) % 16) return fail(FF_ERR_ARG, "tensors must be 16-byte aligned");
   ffKernelConfig cfg = *cfg_in;
-  rc = finish_config(ch, &cfg);
+  rc = finish_config(ch, &cfg, num_sms_cached());
   if (rc) return rc;
-  const size_t need = ff_chain_workspace_bytes(ch, &cfg);
+  const size_t need = ws_layout(ch, &cfg).total;
   if (need && (ws == nullptr || ws_bytes < need)) return fail(FF_ERR_ARG, "workspace too small");
-  LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb);
+  if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(FF_ERR_ARG, "workspace must be 256-byte aligned");
+  LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb, cfg.exchange);
   return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -6,27 +6,35 @@
 // Reference semantics: fuseplan simulator.execute_plan (simulator.py:177-424)
 // and the dsm_comm primitives it models (analyzer.py:331-354).
 //
-// Decomposition (one cluster = one shuffle ring of G CTAs, cls_shuffle = G):
-//   * every CTA owns 128 rows of M (tcgen05 M=128, TMEM lane = row) and a
-//     kLB-wide column slice of E that it accumulates in TMEM for the whole
-//     N range of its split (the E tile never leaves the SM until the store);
-//   * N is walked in "n-steps" of G*kNB columns.  In n-step t, ring member p
-//     runs GEMM0 for its own kNB-wide chunk of the intermediate C (TMEM C
-//     accumulator, double buffered across n-steps), applies the activation /
-//     SwiGLU gate and writes bf16 C into shared memory in the UMMA K-major
-//     128B-swizzled layout (so the tile is directly the A operand of GEMM1);
-//   * dsm_shuffle: every chunk is pushed over distributed shared memory to
-//     the other G-1 ring members (cp.async.bulk shared::cta -> shared::cluster
-//     with mbarrier complete_tx, 2 receive buffers, per-hop credit counters).
-//     At hop h a CTA multiplies the chunk that originated at ring member
-//     (p-h) mod G with the matching D rows into its E tile; the hops of n-step
-//     t are interleaved with the GEMM0 k-blocks of n-step t+1;
-//   * inter-cluster reduce: when N is split across S clusters the E tiles
-//     are combined with red.global.add.v4.f32 into an fp32 workspace, then a
-//     finalize kernel casts to bf16 (simulator.py:371 "+=" into E).
+// Decomposition.  A "ring" of G CTAs shares the intermediate C of one 128-row
+// M tile (cls_shuffle = G):
+//   * each CTA owns a kLB-wide column slice of E that it accumulates in TMEM
+//     over the whole N range of its split;
+//   * N is walked in n-steps of G*kNB columns.  In n-step t ring member p runs
+//     GEMM0 for its own kNB-wide chunk of C (TMEM accumulator, double
+//     buffered), applies the activation / SwiGLU gate (all_exchange "Mul" of
+//     the two branch accumulators) and writes bf16 C to shared memory in the
+//     UMMA K-major 128B-swizzled layout -- directly the A operand of GEMM1;
+//   * shuffle: every chunk reaches the other G-1 members, which multiply it
+//     with the matching D rows into their E slice.  Two transports:
+//       kMode 0 (DSM): cp.async.bulk shared::cta -> shared::cluster pushes
+//         into 2 receive buffers per CTA, mbarrier complete_tx on landing,
+//         counter credits for buffer reuse and landing acks for the source;
+//         the ring is one thread-block cluster;
+//       kMode 1 (L2): the chunk is TMA-stored to an L2-resident scratch and
+//         the members TMA-load it as GEMM1's A operand; a per-chunk epoch
+//         flag (st.release / ld.acquire, gpu scope) orders store and loads.
+//         Requires a fully co-resident (cooperative) launch.
+//     GEMM1 hops of n-step t are interleaved with GEMM0 k-blocks of n-step t+1;
+//   * inter-cluster reduce: with S > 1 N splits the E tiles are combined with
+//     red.global.add.v4.f32 into an fp32 workspace, then cast to bf16
+//     (simulator.py:371 "+=" into E); with S == 1 E is stored in bf16;
+//   * persistent: each ring processes work units (m tile, l cluster, split)
+//     unit = ring_id, ring_id + n_rings, ...; every counter is global across
+//     units so the pipelines never drain between units.
 //
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (+TMEM alloc),
-// w2 DSM push driver, w3 DSM buffer recycler / credits, w4..w7 epilogue.
+// w2 DSM push driver, w3 DSM receive recycler, w4..w7 epilogue.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -36,19 +44,23 @@
 namespace ff {
 
 enum Act : int { ACT_IDENTITY = 0, ACT_RELU = 1, ACT_SILU = 2, ACT_GELU_TANH = 3 };
+enum Xchg : int { XCHG_DSM = 0, XCHG_L2 = 1 };
 
 struct ChainArgs {
   int M, N, K, L;
-  int G;               // ring size (CTAs per cluster)
-  int S;               // N splits across clusters
+  int G;               // ring size
+  int S;               // N splits
   int steps;           // n-steps per split
   int m_tiles;         // ceil(M / 128)
   int l_clusters;      // L / (G * LB)
+  int n_units;         // m_tiles * l_clusters * S
+  int n_rings;         // rings launched (persistent)
   int act;
-  __nv_bfloat16* E;    // output (used when S == 1)
-  float* ws;           // fp32 accumulation workspace (used when S > 1)
+  uint32_t epoch;      // L2 mode: flag value of this launch (monotonic)
+  __nv_bfloat16* E;    // output (S == 1)
+  float* ws;           // fp32 accumulation workspace (S > 1)
+  uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
-  int dbg;                 // debug switches (FF_DEBUG_FLAGS), 0 in production
 };
 
 __device__ __forceinline__ float apply_act(int act, float x) {
@@ -67,59 +79,68 @@ __device__ __forceinline__ float apply_act(int act, float x) {
   }
 }
 
-template <bool kGated, int kNB, int kLB, int kStages>
+template <bool kGated, int kNB, int kLB, int kStages, int kMode>
 struct ChainCfg {
   static constexpr int BM = 128;
   static constexpr int BK = 64;
-  static constexpr int kCW = kNB;                  // width of one C chunk (columns of C)
+  static constexpr int kCW = kNB;                      // columns of C in one chunk
   static constexpr int kAcc = kGated ? 2 * kNB : kNB;  // TMEM columns per C accumulator buffer
-  static constexpr int kA_BYTES = BM * BK * 2;     // 16 KB
+  static constexpr int kA_BYTES = BM * BK * 2;         // 16 KB (A tile, or a C tile in L2 mode)
   static constexpr int kB_BYTES = (kGated ? 2 : 1) * BK * kNB * 2;
   static constexpr int kD_BYTES = BK * kLB * 2;
   static constexpr int kG0_BYTES = kA_BYTES + kB_BYTES;
-  static constexpr int kSTAGE = kG0_BYTES > kD_BYTES ? kG0_BYTES : kD_BYTES;
-  static constexpr int kCHUNK_BYTES = BM * kCW * 2;  // one bf16 C chunk
+  static constexpr int kG1_BYTES = (kMode == XCHG_L2 ? kA_BYTES : 0) + kD_BYTES;
+  static constexpr int kG1_DOFF = (kMode == XCHG_L2 ? kA_BYTES : 0);  // D offset inside a stage
+  static constexpr int kSTAGE = kG0_BYTES > kG1_BYTES ? kG0_BYTES : kG1_BYTES;
+  static constexpr int kCHUNK_BYTES = BM * kCW * 2;
+  static constexpr int kRECV = (kMode == XCHG_DSM) ? 2 : 0;
   static constexpr int kOFF_OWN = kStages * kSTAGE;
   static constexpr int kOFF_RECV = kOFF_OWN + kCHUNK_BYTES;
-  static constexpr int kOFF_BAR = kOFF_RECV + 2 * kCHUNK_BYTES;
-  static constexpr int kNUM_BARS = 2 * kStages + 13 + 9;  // 13 named barriers + 16 u32 credit counters
+  static constexpr int kOFF_BAR = kOFF_RECV + kRECV * kCHUNK_BYTES;
+  static constexpr int kNUM_BARS = 2 * kStages + 13 + 9;  // 13 named barriers + 16 u32 counters
   static constexpr int kSMEM = kOFF_BAR + kNUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
-  static constexpr int kTMEM_E = 2 * kAcc;          // E accumulator column offset
+  static constexpr int kTMEM_E = 2 * kAcc;
   static constexpr int kTMEM_COLS = 512;
   static_assert(2 * kAcc + kLB <= 512, "TMEM budget");
   static_assert(kCW % 64 == 0 && kLB % 64 == 0 && kLB <= 256, "tile shape");
   static_assert(kSTAGE % 1024 == 0 && kCHUNK_BYTES % 1024 == 0, "1024B alignment for SW128");
 };
 
-template <bool kGated, int kNB, int kLB, int kStages>
+template <bool kGated, int kNB, int kLB, int kStages, int kMode>
 __global__ void __launch_bounds__(256, 1)
     ff_chain_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
-                    const ChainArgs args) {
-  using C = ChainCfg<kGated, kNB, kLB, kStages>;
+                    const __grid_constant__ CUtensorMap tmC, const ChainArgs args) {
+  using C = ChainCfg<kGated, kNB, kLB, kStages, kMode>;
+  constexpr bool kDSM = (kMode == XCHG_DSM);
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte alignment for the 128B swizzle atoms.
   const uint32_t raw_base = smem_u32(smem_raw);
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
   const int warp = threadIdx.x / 32;
-  const uint32_t p = cluster_rank();  // ring position
   const int G = args.G;
-
-  // cluster -> (m tile, l cluster, n split); m fastest so concurrent clusters share weight tiles in L2
-  const int cidx = blockIdx.x / G;
-  const int mt = cidx % args.m_tiles;
-  const int rest = cidx / args.m_tiles;
-  const int lc = rest % args.l_clusters;
-  const int split = rest / args.l_clusters;
-  const int m0 = mt * C::BM;
-  const int l0 = (lc * G + (int)p) * kLB;
-  const int n_split0 = split * args.steps * G * kNB;
+  const uint32_t p = kDSM ? cluster_rank() : (uint32_t)(blockIdx.x % G);  // ring position
+  const int ring = blockIdx.x / G;
   const int kblocks = args.K / C::BK;
   const int steps = args.steps;
+  // units processed by this ring; the flat list of (unit, n-step) is the "global step" T
+  const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
+  const int total_steps = my_units * steps;
 
-  // barrier addresses
+  struct Unit {
+    int m0, l0, n0, id;
+  };
+  auto unit_of = [&](int i) {  // i-th unit of this ring
+    const int u = ring + i * args.n_rings;
+    const int mt = u % args.m_tiles;
+    const int rest = u / args.m_tiles;
+    const int lc = rest % args.l_clusters;
+    const int split = rest / args.l_clusters;
+    return Unit{mt * C::BM, (lc * G + (int)p) * kLB, split * steps * G * kNB, u};
+  };
+
+  // barriers
   const uint32_t bar0 = base + C::kOFF_BAR;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
@@ -129,9 +150,9 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t own_full = bx + 32, own_free = bx + 40;
   const uint32_t recv_full[2] = {bx + 48, bx + 56};
   const uint32_t recv_used[2] = {bx + 64, bx + 72};
-  const uint32_t e_full = bx + 96;
-  auto credit = [&](int h) { return bx + 104 + 4u * h; };  // u32 counters, h = 1..G-1
-  const uint32_t ack_count = credit(0);  // landed-chunk acknowledgements from receivers
+  const uint32_t e_full = bx + 80, e_empty = bx + 88;
+  auto counter = [&](int h) { return bx + 104 + 4u * h; };  // 16 u32 counters
+  const uint32_t ack_count = counter(0);                    // DSM: landed-chunk acks
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
   const uint32_t own_slot = base + C::kOFF_OWN;
   const uint32_t recv_slot[2] = {base + C::kOFF_RECV, base + C::kOFF_RECV + C::kCHUNK_BYTES};
@@ -147,26 +168,37 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(recv_full[b], 1);
       mbar_init(recv_used[b], 1);
     }
-    for (int h = 0; h < 16; ++h) *reinterpret_cast<volatile uint32_t*>(smem_gen + (credit(h) - base)) = 0u;
+    for (int h = 0; h < 16; ++h) *reinterpret_cast<volatile uint32_t*>(smem_gen + (counter(h) - base)) = 0u;
     mbar_init(own_full, 128);
-    mbar_init(own_free, G > 1 ? 2 : 1);
+    // own slot reusable after: MMA hop 0 commit + (DSM: all pushes acked | L2: TMA store done)
+    mbar_init(own_free, G == 1 ? 1 : 2);
     mbar_init(e_full, 1);
+    mbar_init(e_empty, 128);
     fence_mbar_init();
-    // receive buffers armed for their first use
-    for (int b = 0; b < 2; ++b) mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
+    if (kDSM)
+      for (int b = 0; b < 2; ++b) mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
   }
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB0);
     if (kGated) tma_prefetch_desc(&tmB1);
     tma_prefetch_desc(&tmD);
+    if (!kDSM && G > 1) tma_prefetch_desc(&tmC);
   }
   if (warp == 1) tmem_alloc<C::kTMEM_COLS>(tmem_slot);
   tc_fence_before();
-  // barriers of every CTA must be initialised before any peer pushes into them
-  cluster_sync();
+  if (kDSM)
+    cluster_sync();  // peers push into our buffers only after our barriers exist
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+
+  // slot h of global step T holds GEMM0 k-blocks [h*KB/G, (h+1)*KB/G) of step T+1
+  auto slot_lo = [&](int h) { return h * kblocks / G; };
+  auto flag_addr = [&](const Unit& u, int t, int origin) {
+    return args.flags + ((size_t)u.id * steps + t) * G + origin;
+  };
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -178,15 +210,14 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
-      // Loads follow the MMA issue order exactly: GEMM0(t+1) k-blocks are
-      // interleaved with GEMM1(t) ring hops (slot h = k-blocks [h*KB/G, (h+1)*KB/G)).
-      auto load_gemm0 = [&](int t, int kb0, int kb1) {
-        const int n0 = n_split0 + (t * G + (int)p) * kNB;
+      auto load_gemm0 = [&](int T, int kb0, int kb1) {
+        const Unit u = unit_of(T / steps);
+        const int n0 = u.n0 + ((T % steps) * G + (int)p) * kNB;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);
-          tma_load_2d(sb, &tmA, full_bar(stage), kb * C::BK, m0);
+          tma_load_2d(sb, &tmA, full_bar(stage), kb * C::BK, u.m0);
           if (kGated) {
             tma_load_2d(sb + C::kA_BYTES, &tmB0, full_bar(stage), n0, kb * C::BK);
             tma_load_2d(sb + C::kA_BYTES + C::BK * kNB * 2, &tmB1, full_bar(stage), n0, kb * C::BK);
@@ -198,26 +229,37 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
       };
-      auto load_hop = [&](int t, int h) {
+      auto load_hop = [&](int T, int h) {
+        const Unit u = unit_of(T / steps);
+        const int t = T % steps;
         const int origin = ((int)p - h + G) % G;
-        const int nrow0 = n_split0 + (t * G + origin) * kNB;
+        const int nrow0 = u.n0 + (t * G + origin) * kNB;
+        const bool remote_c = !kDSM && h > 0;
+        if (remote_c) {
+          // wait until ring member `origin` published chunk (unit, t)
+          const uint32_t* f = flag_addr(u, t, origin);
+          uint32_t polls = 0;
+          while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+          }
+          fence_proxy_async_global();
+        }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sb = base + stage * C::kSTAGE;
-          mbar_expect_tx(full_bar(stage), C::kD_BYTES);
+          mbar_expect_tx(full_bar(stage), remote_c ? C::kG1_BYTES : C::kD_BYTES);
+          if (remote_c) tma_load_2d(sb, &tmC, full_bar(stage), nrow0 + kb2 * C::BK, u.m0);
 #pragma unroll
           for (int j = 0; j < kLB / 64; ++j)
-            tma_load_2d(sb + j * 8192, &tmD, full_bar(stage), l0 + 64 * j, nrow0 + kb2 * C::BK);
+            tma_load_2d(sb + C::kG1_DOFF + j * 8192, &tmD, full_bar(stage), u.l0 + 64 * j, nrow0 + kb2 * C::BK);
           next();
         }
       };
-      load_gemm0(0, 0, kblocks);
-      for (int t = 0; t < steps; ++t) {
+      if (total_steps > 0) load_gemm0(0, 0, kblocks);
+      for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
-          const int s0 = (args.dbg & 8) ? (h ? kblocks : 0) : h * kblocks / G;
-          const int s1 = (args.dbg & 8) ? kblocks : (h + 1) * kblocks / G;
-          if (t + 1 < steps) load_gemm0(t + 1, s0, s1);
-          load_hop(t, h);
+          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          load_hop(T, h);
         }
       }
     }
@@ -233,10 +275,10 @@ __global__ void __launch_bounds__(256, 1)
       };
       constexpr uint32_t idesc0 = idesc_bf16(128, kNB, 0, 1);
       constexpr uint32_t idesc1 = idesc_bf16(128, kLB, 0, 1);
-      auto gemm0 = [&](int t, int kb0, int kb1) {
-        const int cb = t & 1;
+      auto gemm0 = [&](int T, int kb0, int kb1) {
+        const int cb = T & 1;
         if (kb0 == 0) {
-          mbar_wait(c_empty[cb], ((t >> 1) & 1) ^ 1);
+          mbar_wait(c_empty[cb], ((T >> 1) & 1) ^ 1);
           tc_fence_after();
         }
         const uint32_t tacc = tmem_base + cb * C::kAcc;
@@ -265,27 +307,38 @@ __global__ void __launch_bounds__(256, 1)
       };
       int ri = 0;
       bool e_started = false;
-      auto hop = [&](int t, int h) {
-        uint32_t slot;
+      auto hop = [&](int T, int h) {
+        const int t = T % steps;
+        if (t == 0 && h == 0) {
+          // new unit: the epilogue must have drained the previous unit's E tile
+          const int ui = T / steps;
+          if (ui > 0) {
+            mbar_wait(e_empty, (ui - 1) & 1);
+            tc_fence_after();
+          }
+          e_started = false;
+        }
+        uint32_t slot = 0;
         int b = 0;
         if (h == 0) {
-          mbar_wait(own_full, t & 1);
+          mbar_wait(own_full, T & 1);
           slot = own_slot;
-        } else {
+        } else if (kDSM) {
           b = ri & 1;
           mbar_wait_cluster(recv_full[b], (ri >> 1) & 1);
           slot = recv_slot[b];
         }
         tc_fence_after();
+        const bool from_stage = !kDSM && h > 0;
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           mbar_wait(full_bar(stage), phase);
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t ab = slot + kb2 * (C::BM * C::BK * 2);
+          const uint32_t ab = from_stage ? sb : slot + kb2 * (C::BM * C::BK * 2);
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             const uint64_t ad = desc_kmajor_sw128(ab + kk * 32);
-            const uint64_t bd = desc_mnmajor_sw128(sb + kk * 2048, 8192);
+            const uint64_t bd = desc_mnmajor_sw128(sb + C::kG1_DOFF + kk * 2048, 8192);
             umma_bf16(tmem_base + C::kTMEM_E, ad, bd, idesc1, e_started ? 1u : 0u);
             e_started = true;
           }
@@ -294,69 +347,60 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (h == 0) {
           umma_commit(own_free);
-        } else {
+        } else if (kDSM) {
           umma_commit(recv_used[b]);
           ++ri;
         }
+        if (t == steps - 1 && h == G - 1) umma_commit(e_full);
       };
-      gemm0(0, 0, kblocks);
-      for (int t = 0; t < steps; ++t) {
+      if (total_steps > 0) gemm0(0, 0, kblocks);
+      for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
-          const int s0 = (args.dbg & 8) ? (h ? kblocks : 0) : h * kblocks / G;
-          const int s1 = (args.dbg & 8) ? kblocks : (h + 1) * kblocks / G;
-          if (t + 1 < steps) gemm0(t + 1, s0, s1);
-          hop(t, h);
+          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          hop(T, h);
         }
       }
-      umma_commit(e_full);
     }
   } else if (warp == 2) {
-    // ============ dsm_shuffle, send side: direct pushes of the own chunk ============
-    // At hop h ring member q consumes the chunk of origin (q-h) mod G, so origin
-    // p pushes its chunk to (p+h) mod G in hop order; no store-and-forward chain.
-    // Receiver q's global receive index R = t*(G-1) + h-1 selects buffer R & 1;
-    // reusing a buffer needs a credit (remote increment of counter h) sent by
-    // the receiver once it consumed receive R-2.
-    if (G > 1 && elect_one()) {
-      for (int t = 0; t < steps; ++t) {
-        mbar_wait(own_full, t & 1);
+    // ===== DSM shuffle, send side: direct pushes of the own chunk (kMode 0) =====
+    // At hop h ring member q consumes the chunk of origin (q-h) mod G, so
+    // origin p pushes to (p+h) mod G in hop order.  Receiver q's global receive
+    // index R = T*(G-1) + h-1 selects buffer R & 1; reusing a buffer needs a
+    // credit (remote increment of counter h) sent once q consumed receive R-2.
+    if (kDSM && G > 1 && elect_one()) {
+      for (int T = 0; T < total_steps; ++T) {
+        mbar_wait(own_full, T & 1);
         for (int h = 1; h < G; ++h) {
           const uint32_t dest = (p + h) % G;
-          const int R = t * (G - 1) + h - 1;
+          const int R = T * (G - 1) + h - 1;
           if (R >= 2) {
-            // credits on counter h arrive once per step from step `first` on
             const int first = (3 - h) <= 0 ? 0 : (3 - h + G - 2) / (G - 1);
-            credit_wait(credit(h), (uint32_t)(t - first + 1));
+            credit_wait(counter(h), (uint32_t)(T - first + 1));
           }
-          if (args.dbg & 2) asm volatile("fence.proxy.async;" ::: "memory");
           const int b = R & 1;
           dsm_bulk_push(mapa(recv_slot[b], dest), own_slot, C::kCHUNK_BYTES, mapa(recv_full[b], dest));
         }
-        // A shared::cta -> shared::cluster bulk copy completes only through the
-        // destination's mbarrier (it is not a bulk-group op), so the own slot is
-        // free once every receiver acknowledged that its copy landed.
-        credit_wait(ack_count, (uint32_t)((t + 1) * (G - 1)));
+        // a shared::cta -> shared::cluster bulk copy completes only through the
+        // destination's mbarrier, so the own slot is free once all receivers acked.
+        credit_wait(ack_count, (uint32_t)((T + 1) * (G - 1)));
         mbar_arrive(own_free);
       }
     }
   } else if (warp == 3) {
-    // ============ dsm_shuffle, receive side: recycle buffers, credit the next writer ============
-    if (G > 1 && elect_one()) {
-      const int total = steps * (G - 1);
+    // ===== DSM shuffle, receive side: ack landing, recycle, credit (kMode 0) =====
+    if (kDSM && G > 1 && elect_one()) {
+      const int total = total_steps * (G - 1);
       for (int R = 0; R < total; ++R) {
         const int b = R & 1;
         const uint32_t ph = (R >> 1) & 1;
-        // landed: acknowledge to the origin so it may overwrite its own slot
         mbar_wait_cluster(recv_full[b], ph);
         const int h = R % (G - 1) + 1;
         credit_add_remote(mapa(ack_count, (p + G - h) % G));
-        // consumed: re-arm the buffer and credit the writer of receive R+2
         mbar_wait(recv_used[b], ph);
         if (R + 2 < total) {
           mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
           const int hn = (R + 2) % (G - 1) + 1;
-          const uint32_t writer = (p + G - hn) % G;
-          credit_add_remote(mapa(credit(hn), writer));
+          credit_add_remote(mapa(counter(hn), (p + G - hn) % G));
         }
       }
     }
@@ -365,26 +409,23 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + (int)lane_id();
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-    for (int t = 0; t < steps; ++t) {
-      const int cb = t & 1;
-      mbar_wait(c_full[cb], (t >> 1) & 1);
+    for (int T = 0; T < total_steps; ++T) {
+      const Unit u = unit_of(T / steps);
+      const int t = T % steps;
+      const int cb = T & 1;
+      mbar_wait(c_full[cb], (T >> 1) & 1);
       tc_fence_after();
-      mbar_wait(own_free, (t & 1) ^ 1);
-      if (args.dbg & 4) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < 40000) {
-        }
-      }
+      mbar_wait(own_free, (T & 1) ^ 1);
       const uint32_t tacc = lane_base + cb * C::kAcc;
 #pragma unroll 1
       for (int c0 = 0; c0 < C::kCW; c0 += 16) {
         float v[16];
         tmem_ld16(tacc + c0, v);
         if (kGated) {
-          float u[16];
-          tmem_ld16(tacc + kNB + c0, u);
+          float w[16];
+          tmem_ld16(tacc + kNB + c0, w);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (v[i] / (1.0f + __expf(-v[i]))) * u[i];
+          for (int i = 0; i < 16; ++i) v[i] = (v[i] / (1.0f + __expf(-v[i]))) * w[i];
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] = apply_act(args.act, v[i]);
@@ -393,13 +434,13 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
         const int sub = c0 / 64;
-        const int ch = (c0 % 64) / 8;  // 16-byte chunk index inside the 128-byte row
+        const int ch = (c0 % 64) / 8;  // 16-byte chunk inside the 128-byte row
         const uint32_t rowb = own_slot + sub * (C::BM * C::BK * 2) + row * 128;
-        st_shared_v4(rowb + (((ch) ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+        st_shared_v4(rowb + ((ch ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
         st_shared_v4(rowb + (((ch + 1) ^ (row & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
-        if (args.c_debug != nullptr && m0 + row < args.M) {
-          const int ncol = n_split0 + (t * G + (int)p) * kNB + c0;
-          uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)(m0 + row) * args.N + ncol);
+        if (args.c_debug != nullptr && u.m0 + row < args.M) {
+          const int ncol = u.n0 + (t * G + (int)p) * kNB + c0;
+          uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)(u.m0 + row) * args.N + ncol);
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
@@ -408,36 +449,53 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive(c_empty[cb]);
       fence_proxy_async_smem();
       mbar_arrive(own_full);
-    }
-    // E tile: TMEM -> registers -> global (bf16 store, or fp32 reduce-add across splits)
-    mbar_wait(e_full, 0);
-    tc_fence_after();
-    const int grow = m0 + row;
-#pragma unroll 1
-    for (int c0 = 0; c0 < kLB; c0 += 16) {
-      float v[16];
-      tmem_ld16(lane_base + C::kTMEM_E + c0, v);
-      if (grow < args.M) {
-        if (args.S == 1) {
-          uint32_t pk[8];
+      if (!kDSM && G > 1) {
+        // publish the chunk through L2: TMA store, then release the ready flag
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane_id() == 0) {
+          const int ncol = u.n0 + (t * G + (int)p) * kNB;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-          uint4* dst = reinterpret_cast<uint4*>(args.E + (size_t)grow * args.L + l0 + c0);
-          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        } else {
-          float* dst = args.ws + (size_t)grow * args.L + l0 + c0;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) red_add_v4_f32(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+          for (int sub = 0; sub < C::kCW / 64; ++sub)
+            tma_store_2d(&tmC, own_slot + sub * (C::BM * C::BK * 2), ncol + 64 * sub, u.m0);
+          bulk_commit();
+          bulk_wait0();
+          fence_proxy_async_global();
+          st_release_gpu_u32(flag_addr(u, t, (int)p), args.epoch);
+          mbar_arrive(own_free);
         }
       }
+      if (t == steps - 1) {
+        // E tile of this unit: TMEM -> registers -> global
+        mbar_wait(e_full, (T / steps) & 1);
+        tc_fence_after();
+        const int grow = u.m0 + row;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kLB; c0 += 16) {
+          float v[16];
+          tmem_ld16(lane_base + C::kTMEM_E + c0, v);
+          if (grow < args.M) {
+            if (args.S == 1) {
+              uint32_t pk[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              uint4* dst = reinterpret_cast<uint4*>(args.E + (size_t)grow * args.L + u.l0 + c0);
+              dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            } else {
+              float* dst = args.ws + (size_t)grow * args.L + u.l0 + c0;
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) red_add_v4_f32(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(e_empty);
+      }
     }
-    tc_fence_before();
   }
 
   __syncthreads();
-  // no CTA may leave while a ring neighbour can still push into it or credit it
-  cluster_sync();
+  if (kDSM) cluster_sync();  // no CTA leaves while a peer may still push or credit
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kTMEM_COLS>(tmem_base);

@@ -139,6 +139,20 @@ __device__ __forceinline__ void credit_wait(uint32_t addr, uint32_t target) {
   }
 }
 
+// gpu-scope release/acquire flags in global memory
+__device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// named barrier among `count` threads
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ----------------------------------------------------------------------------
 // fences
 // ----------------------------------------------------------------------------
@@ -184,7 +198,16 @@ __device__ __forceinline__ void dsm_bulk_push(uint32_t dst_cluster, uint32_t src
       "r"(src_local), "r"(bytes), "r"(dst_bar_cluster)
       : "memory");
 }
+// TMA store (shared -> global); a bulk-group operation.
+__device__ __forceinline__ void tma_store_2d(const void* desc, uint32_t src, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(desc),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+// Bulk-group completion (TMA stores / bulk_group copies only -- NOT the
+// mbarrier-completed shared::cluster copies).
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }

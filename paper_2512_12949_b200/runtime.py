@@ -44,18 +44,25 @@ def _num_sms() -> int:
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
-def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None) -> nat.KernelConfig:
-    """Physical launch configuration for (graph, plan); plan=None lets the
-    runtime choose the hardware-shaped configuration."""
+EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2}
+
+
+def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None,
+          exchange: str = "l2") -> nat.KernelConfig:
+    """Physical launch configuration for (graph, plan).  plan=None lets the
+    runtime choose the hardware-shaped configuration; ``exchange`` picks the
+    shuffle transport: "dsm" (thread-block cluster, distributed shared memory)
+    or "l2" (TMA through an L2-resident scratch)."""
     lib = nat.load()
     cfg = nat.KernelConfig()
     ch = chain_desc(graph)
     sms = num_sms if num_sms is not None else 148
+    x = EXCHANGES[exchange]
     if plan is None:
-        nat.check(lib.ff_auto_config(ctypes.byref(ch), sms, ctypes.byref(cfg)))
+        nat.check(lib.ff_auto_config_ex(ctypes.byref(ch), sms, x, ctypes.byref(cfg)))
     else:
         pd = plan_desc(plan)
-        nat.check(lib.ff_plan_lower(ctypes.byref(ch), ctypes.byref(pd), sms, ctypes.byref(cfg)))
+        nat.check(lib.ff_plan_lower_ex(ctypes.byref(ch), ctypes.byref(pd), sms, x, ctypes.byref(cfg)))
     return cfg
 
 
@@ -67,7 +74,8 @@ def _workspace(nbytes: int, device):
     key = (device.index if device.index is not None else torch.cuda.current_device())
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        # zero-filled once (epoch-stamped flags never need clearing again)
+        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         _workspaces[key] = buf
     return buf
 
@@ -107,9 +115,10 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
     return out
 
 
-def run(graph: ChainGraph, plan: Optional[FusionPlan], tensors: dict, out=None, stream=None):
+def run(graph: ChainGraph, plan: Optional[FusionPlan], tensors: dict, out=None, stream=None,
+        exchange: str = "l2"):
     """Execute the chain under ``plan`` on the current GPU; returns E (bf16)."""
-    return launch(graph, lower(graph, plan, _num_sms()), tensors, out=out, stream=stream)
+    return launch(graph, lower(graph, plan, _num_sms(), exchange), tensors, out=out, stream=stream)
 
 
 def kernel_launches(graph: ChainGraph, cfg: nat.KernelConfig) -> int:
@@ -119,18 +128,24 @@ def kernel_launches(graph: ChainGraph, cfg: nat.KernelConfig) -> int:
     return int(lib.ff_chain_kernel_count(ctypes.byref(ch), ctypes.byref(cfg)))
 
 
-def profile_best_from_list(graph: ChainGraph, plans, tensors: dict, iters: int = 10, warmup: int = 3):
+def profile_best_from_list(graph: ChainGraph, plans, tensors: dict, iters: int = 10, warmup: int = 3,
+                           exchanges=("l2", "dsm")):
     """Alg. 2 line 10 (ProfileBestFromList): time each candidate
-    plan's fused kernel on the device and return [(ms, plan, cfg)] fastest first.
-    Plans with no sm_100a lowering are skipped."""
+    plan's fused kernel (under each shuffle transport) on the device and return
+    [(ms, plan, cfg)] fastest first.  Plans with no sm_100a lowering are skipped."""
     import torch
 
     timed = []
-    for plan in plans:
+    seen = set()
+    for plan, exchange in ((p, x) for p in plans for x in exchanges):
         try:
-            cfg = lower(graph, plan, _num_sms())
+            cfg = lower(graph, plan, _num_sms(), exchange)
         except nat.UnsupportedPlan:
             continue
+        key = tuple(cfg.as_dict().items())
+        if key in seen:
+            continue
+        seen.add(key)
         out = torch.empty((graph.dims.m, graph.dims.l), dtype=torch.bfloat16, device="cuda")
         for _ in range(warmup):
             launch(graph, cfg, tensors, out=out)
