@@ -1,0 +1,25 @@
+"""One fused launch + one cuBLAS unfused chain per workload (for ncu)."""
+import sys, torch
+sys.path.insert(0, '.')
+import bench
+from paper_2512_12949_b200 import runtime
+names = sys.argv[1:] or ["llama1b"]
+for name in names:
+    kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
+    t = bench.make_device_inputs(kind, m, n, k, l, 3, "cuda")
+    g = bench.graph_of(name)
+    cfg = runtime.lower(g, None, 148, "l2")
+    out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for i in range(3):
+        flush.add_(1.0)
+        runtime.launch(g, cfg, t, out=out)
+    f = torch.nn.functional
+    for i in range(2):
+        flush.add_(1.0)
+        if kind == "gated_ffn":
+            r = (f.silu(t["A"] @ t["B0"]) * (t["A"] @ t["B1"])) @ t["D"]
+        else:
+            r = torch.relu(t["A"] @ t["B"]) @ t["D"]
+    torch.cuda.synchronize()
+    print(name, "done", flush=True)
