@@ -74,6 +74,7 @@ typedef struct ffPlanDesc {
 /* Shuffle transport of the intermediate C between ring members. */
 #define FF_XCHG_DSM 0 /* distributed shared memory pushes inside a thread-block cluster */
 #define FF_XCHG_L2 1  /* TMA store / TMA load through an L2-resident scratch (cooperative launch) */
+#define FF_XCHG_L2_PAIR 2 /* as FF_XCHG_L2, ring members are CTA pairs issuing cta_group::2 M=256 MMAs */
 
 /* Physical launch configuration produced by the lowering. */
 typedef struct ffKernelConfig {
@@ -134,6 +135,10 @@ int ff_chain_launch_debug(const ffChainDesc* chain, const ffKernelConfig* cfg, c
 
 /* Number of CUDA kernels one ff_chain_launch issues (for launch accounting). */
 int ff_chain_kernel_count(const ffChainDesc* chain, const ffKernelConfig* cfg);
+
+/* Diagnostics: device buffer of unsigned long long[grid_ctas][16] that receives
+ * per-CTA wait-cycle counters on every launch (NULL disables; default). */
+void ff_set_profile_buffer(void* dev_ptr);
 
 /* Thread-local message for the last non-OK status. */
 const char* ff_last_error(void);

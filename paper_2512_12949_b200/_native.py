@@ -26,7 +26,7 @@ FF_ERR_ARG = 5
 KIND = {"standard_ffn": 0, "gated_ffn": 1}
 ACT = {"identity": 0, "relu": 1, "silu": 2, "gelu": 3}
 LOWERING = {"n/a": 0, "spatial_split": 1, "doubled_k": 2}
-XCHG_DSM, XCHG_L2 = 0, 1
+XCHG_DSM, XCHG_L2, XCHG_L2_PAIR = 0, 1, 2
 
 # Exported symbols (must match include/ff_chain.h).
 EXPORTS = (
@@ -39,6 +39,7 @@ EXPORTS = (
     "ff_chain_run_plan",
     "ff_chain_launch_debug",
     "ff_chain_kernel_count",
+    "ff_set_profile_buffer",
     "ff_last_error",
     "ff_version",
 )
@@ -137,6 +138,7 @@ def load(path: str = LIB_PATH):
         lib.ff_chain_launch_debug.argtypes = [P(ChainDesc), P(KernelConfig), P(Tensors), ctypes.c_void_p,
                                               ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
         lib.ff_chain_kernel_count.argtypes = [P(ChainDesc), P(KernelConfig)]
+        lib.ff_set_profile_buffer.argtypes = [ctypes.c_void_p]
         lib.ff_last_error.restype = ctypes.c_char_p
         lib.ff_version.restype = ctypes.c_char_p
         _lib = lib

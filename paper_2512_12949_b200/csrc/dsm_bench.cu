@@ -4,6 +4,7 @@
 // cp.async.bulk shared::cta -> shared::cluster (mbarrier complete_tx),
 // keeping `depth` transfers in flight.  Reports aggregate bytes/s.
 // Used to calibrate dsm.bandwidth[n] of the B200 device profile.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -135,3 +136,114 @@ int ff_max_active_clusters(int cluster, int smem_bytes, int* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// TMA streaming microbenchmark: each CTA streams `per_cta_kb` k-blocks of a
+// row-major bf16 matrix [rows][cols] through a `stages`-deep ring of 32 KB
+// stages (box = 64 cols x 64 rows MN-major, or 64 cols x 128 rows), the
+// consumer only waits and releases.  Measures per-SM TMA ingress.
+// ---------------------------------------------------------------------------
+namespace {
+// `producers` threads (one per warp) each own stages p, p+P, ... of a ring of
+// `stages` x `stage_bytes` buffers; one consumer thread per producer.
+__global__ void __launch_bounds__(256, 1) tma_stream_kernel(const __grid_constant__ CUtensorMap map, int rows,
+                                                            int cols, int stages, int iters, int box_rows,
+                                                            int producers, int stage_bytes) {
+  using namespace ff;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
+  const uint32_t full0 = base + stages * stage_bytes, empty0 = full0 + 8 * stages;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int box_blocks = box_rows >> 16;
+  box_rows &= 0xffff;
+  const int per_box = 64 * box_rows * 2 * (box_blocks ? box_blocks : 1);
+  const int boxes = stage_bytes / per_box;
+  const int col_tiles = cols / (64 * (box_blocks ? box_blocks : 1)), row_tiles = rows / box_rows;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int my_stages = stages / producers;
+  if (lane == 0 && warp < producers) {
+    int k = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      const int stage = warp + k * producers;
+      mbar_wait(empty0 + 8 * stage, phase ^ 1);
+      mbar_expect_tx(full0 + 8 * stage, stage_bytes);
+      for (int b = 0; b < boxes; ++b) {
+        const long long lin = ((long long)(blockIdx.x * producers + warp) * 7919 + (long long)i * boxes + b);
+        const int ct = (int)(lin % col_tiles), rt = (int)((lin / col_tiles) % row_tiles);
+        if (box_blocks)
+          tma_load_3d(base + stage * stage_bytes + b * per_box, &map, full0 + 8 * stage, 0, rt * box_rows,
+                      ct * box_blocks);
+        else
+          tma_load_2d(base + stage * stage_bytes + b * per_box, &map, full0 + 8 * stage, ct * 64, rt * box_rows);
+      }
+      if (++k == my_stages) { k = 0; phase ^= 1; }
+    }
+  } else if (lane == 0 && warp >= 4 && warp - 4 < producers) {
+    const int w = warp - 4;
+    int k = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      const int stage = w + k * producers;
+      mbar_wait(full0 + 8 * stage, phase);
+      mbar_arrive(empty0 + 8 * stage);
+      if (++k == my_stages) { k = 0; phase ^= 1; }
+    }
+  }
+  __syncthreads();
+}
+}  // namespace
+
+extern "C" int ff_tma_stream_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows,
+                                   int ctas, int producers, int stage_bytes, float* ms_out) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) return 4;
+  CUtensorMap map;
+  const int bb = box_rows >> 16, br = box_rows & 0xffff;
+  CUresult cr;
+  if (bb) {
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)cols / 64};
+    cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)br, (cuuint32_t)bb};
+    cuuint32_t estr[3] = {1, 1, 1};
+    cr = reinterpret_cast<EncodeFn>(p)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(mat), dims, strides,
+                                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)br};
+    cuuint32_t estr[2] = {1, 1};
+    cr = reinterpret_cast<EncodeFn>(p)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(mat), dims, strides,
+                                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (cr != CUDA_SUCCESS) return 6;
+  const int smem = stages * stage_bytes + 16 * stages + 2048;
+  if (smem > 232448) return 5;
+  cudaFuncSetAttribute(tma_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  tma_stream_kernel<<<ctas, 256, smem>>>(map, rows, cols, stages, 8, box_rows, producers, stage_bytes);
+  cudaEventRecord(a);
+  tma_stream_kernel<<<ctas, 256, smem>>>(map, rows, cols, stages, iters, box_rows, producers, stage_bytes);
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) return 4;
+  *ms_out = ms;
+  return 0;
+}

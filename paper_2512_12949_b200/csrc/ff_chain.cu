@@ -13,6 +13,7 @@
 
 #include "../../include/ff_chain.h"
 #include "ff_chain_kernel.cuh"
+#include "ff_chain_pair_kernel.cuh"
 
 namespace {
 
@@ -104,17 +105,20 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   size_t off = 0;
   w.e_off = off;
   if (c->n_splits > 1) off = align256(off + (size_t)ch->m * ch->l * sizeof(float));
+  const bool pair = c->exchange == FF_XCHG_L2_PAIR;
   w.c_off = off;
-  if (c->exchange == FF_XCHG_L2 && c->ring > 1) {
-    off = align256(off + (size_t)c->m_tiles * 128 * ch->n * 2);
+  if (c->exchange != FF_XCHG_DSM && c->ring > 1) {
+    off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   }
   w.f_off = off;
-  if (c->exchange == FF_XCHG_L2) off = align256(off + (size_t)c->units * c->steps * c->ring * sizeof(uint32_t));
+  if (c->exchange != FF_XCHG_DSM)
+    off = align256(off + (size_t)c->units * c->steps * c->ring * (pair ? 2 : 1) * sizeof(uint32_t));
   w.total = off;
   return w;
 }
 
 std::atomic<uint32_t> g_epoch{0};
+unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA wait-cycle counters (ff_set_profile_buffer)
 
 template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
@@ -175,7 +179,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   }
   lc.gridDim = dim3(rings * cfg->ring, 1, 1);
 
-  ff::ChainArgs a;
+  ff::ChainArgs a{};
   a.M = (int)M;
   a.N = (int)N;
   a.K = (int)K;
@@ -193,6 +197,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
+  a.prof = g_prof;
 
   if (cfg->n_splits > 1) {
     cudaError_t e = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
@@ -210,9 +215,106 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   return FF_OK;
 }
 
+template <bool kGated, int kLB>
+struct PairStages {
+  using Probe = ff::PairCfg<kGated, kLB, 1>;
+  static constexpr int kFixed = Probe::kSMEM - Probe::kSTAGE - 2 * 8;
+  static constexpr int kMax = (232448 - kFixed - 64) / (Probe::kSTAGE + 16);
+  static constexpr int value = kMax > 8 ? 8 : kMax;
+};
+
+template <bool kGated, int kLB>
+int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
+                     cudaStream_t stream) {
+  constexpr int kStages = PairStages<kGated, kLB>::value;
+  static_assert(kStages >= 3, "not enough shared memory for a pipeline");
+  using C = ff::PairCfg<kGated, kLB, kStages>;
+  auto kern = ff::ff_chain_pair_kernel<kGated, kLB, kStages>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM); });
+  if (attr_err != cudaSuccess)
+    return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+
+  const uint64_t M = ch->m, N = ch->n, K = ch->k, L = ch->l;
+  const WsLayout wl = ws_layout(ch, cfg);
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  CUtensorMap mA, mB0, mB1, mD, mC;
+  bool ok = make_map(&mA, t->a, M, K, 64, 128);
+  ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
+  ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
+  ok = ok && make_map(&mD, t->d, N, L, 64, 64);
+  const bool l2x = cfg->ring > 1;
+  ok = ok && make_map(&mC, l2x ? (const void*)(wsb + wl.c_off) : t->a, l2x ? (uint64_t)cfg->m_tiles * 256 : M,
+                      l2x ? N : K, 64, 128);
+  if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
+
+  const int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
+  if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring of pairs larger than the GPU");
+  ff::ChainArgs a{};
+  a.M = (int)M;
+  a.N = (int)N;
+  a.K = (int)K;
+  a.L = (int)L;
+  a.G = cfg->ring;
+  a.S = cfg->n_splits;
+  a.steps = cfg->steps;
+  a.m_tiles = cfg->m_tiles;
+  a.l_clusters = cfg->l_clusters;
+  a.n_units = cfg->units;
+  a.n_rings = rings;
+  a.act = ch->activation;
+  a.epoch = g_epoch.fetch_add(1) + 1;
+  a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
+  a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
+  a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
+  a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
+  a.prof = g_prof;
+  if (cfg->n_splits > 1) {
+    cudaError_t e = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
+    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(rings * cfg->ring * 2, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = C::kSMEM;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
+  if (e != cudaSuccess) {
+    // cooperative + cluster not accepted: the grid is sized to co-residency anyway
+    cudaGetLastError();
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
+  }
+  if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx(pair): ") + cudaGetErrorString(e));
+  if (cfg->n_splits > 1) {
+    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(a.ws, a.E, (size_t)M * L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
+  }
+  return FF_OK;
+}
+
 using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);
 
 LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
+  if (mode == FF_XCHG_L2_PAIR) {
+    if (nb != (gated ? 128 : 256)) return nullptr;
+    if (gated && lb == 256) return &launch_pair_impl<true, 256>;
+    if (gated && lb == 128) return &launch_pair_impl<true, 128>;
+    if (!gated && lb == 256) return &launch_pair_impl<false, 256>;
+    if (!gated && lb == 128) return &launch_pair_impl<false, 128>;
+    return nullptr;
+  }
 #define FF_CASE(G, NB, LB)                                                    \
   if (gated == G && nb == NB && lb == LB)                                     \
     return mode == FF_XCHG_DSM ? &launch_impl<G, NB, LB, ff::XCHG_DSM>        \
@@ -247,8 +349,10 @@ int validate_chain(const ffChainDesc* ch) {
 // Fill derived fields and check that a physical configuration is executable.
 int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const bool gated = ch->kind == FF_KIND_GATED;
-  if (c->exchange != FF_XCHG_DSM && c->exchange != FF_XCHG_L2) return fail(FF_ERR_ARG, "unknown exchange");
-  if (c->ring < 1 || c->ring > (c->exchange == FF_XCHG_DSM ? 16 : num_sms))
+  if (c->exchange != FF_XCHG_DSM && c->exchange != FF_XCHG_L2 && c->exchange != FF_XCHG_L2_PAIR)
+    return fail(FF_ERR_ARG, "unknown exchange");
+  const int width = c->exchange == FF_XCHG_L2_PAIR ? 2 : 1;  // CTAs per ring member
+  if (c->ring < 1 || c->ring > (c->exchange == FF_XCHG_DSM ? 16 : num_sms / width))
     return fail(FF_ERR_UNSUPPORTED, "ring size out of range (DSM rings are clusters of <= 16 CTAs)");
   if (c->n_splits < 1) return fail(FF_ERR_UNSUPPORTED, "n_splits must be >= 1");
   if (!select_kernel(gated, c->nb, c->lb, c->exchange)) return fail(FF_ERR_UNSUPPORTED, "no kernel for (nb, lb)");
@@ -258,13 +362,15 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   if (ch->n % nstep) return fail(FF_ERR_UNSUPPORTED, "n_splits * ring * nb must divide n");
   c->l_clusters = (int32_t)(ch->l / lcover);
   c->steps = (int32_t)(ch->n / nstep);
-  c->m_tiles = (int32_t)((ch->m + 127) / 128);
+  const int rows = 128 * width;
+  c->m_tiles = (int32_t)((ch->m + rows - 1) / rows);
   const int64_t units = (int64_t)c->m_tiles * c->l_clusters * c->n_splits;
   if (units > (1ll << 30)) return fail(FF_ERR_UNSUPPORTED, "grid too large");
   c->units = (int32_t)units;
-  const int64_t max_rings = c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / c->ring;
+  const int64_t max_rings =
+      c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
   c->rings = (int32_t)std::min<int64_t>(units, max_rings);
-  c->grid_ctas = c->rings * c->ring;
+  c->grid_ctas = c->rings * c->ring * width;
   return FF_OK;
 }
 
@@ -276,9 +382,11 @@ int pick_lb(int64_t cover, int max_ring) {
 
 // Grow the number of N splits while the units do not yet fill the co-resident rings.
 void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
-  const int max_rings = c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / c->ring;
+  const int width = c->exchange == FF_XCHG_L2_PAIR ? 2 : 1;
+  const int max_rings =
+      c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
   for (;;) {
-    const int64_t per = (int64_t)((ch->m + 127) / 128) * (ch->l / ((int64_t)c->ring * c->lb));
+    const int64_t per = (int64_t)((ch->m + 128 * width - 1) / (128 * width)) * (ch->l / ((int64_t)c->ring * c->lb));
     const int64_t next = (int64_t)c->n_splits * 2;
     if (per * next > max_rings) break;
     if (ch->n % (next * c->ring * c->nb)) break;
@@ -291,6 +399,10 @@ void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
 extern "C" {
 
 const char* ff_last_error(void) { return g_last_error.c_str(); }
+
+// Diagnostics: when non-NULL, kernels write per-CTA wait-cycle counters
+// (unsigned long long[grid_ctas][16]) into this device buffer.
+void ff_set_profile_buffer(void* dev_ptr) { g_prof = reinterpret_cast<unsigned long long*>(dev_ptr); }
 const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
 
 int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {
@@ -301,12 +413,17 @@ int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, 
   ffKernelConfig c = {};
   c.exchange = exchange;
   const bool gated = ch->kind == FF_KIND_GATED;
-  const int max_ring = exchange == FF_XCHG_DSM ? 16 : num_sms;
+  const int max_ring = exchange == FF_XCHG_DSM ? 16 : (exchange == FF_XCHG_L2_PAIR ? num_sms / 2 : num_sms);
   c.lb = pick_lb(ch->l, max_ring);
   if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "l cannot be covered by one ring");
   c.ring = (int32_t)(ch->l / c.lb);
-  c.nb = gated ? 64 : 128;
-  if (ch->n % ((int64_t)c.ring * c.nb)) c.nb = 64;
+  if (exchange == FF_XCHG_L2_PAIR) {
+    if (c.lb < 128) return fail(FF_ERR_UNSUPPORTED, "pair kernel needs l slices of >= 128 columns");
+    c.nb = gated ? 128 : 256;
+  } else {
+    c.nb = gated ? 64 : 128;
+    if (ch->n % ((int64_t)c.ring * c.nb)) c.nb = 64;
+  }
   c.n_splits = 1;
   fill_machine(ch, &c, num_sms);
   rc = finish_config(ch, &c, num_sms);
@@ -352,16 +469,17 @@ int ff_plan_lower_ex(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_
   ffKernelConfig c = {};
   c.exchange = exchange;
   const int64_t lcover = (int64_t)cl * plan->block[3];
-  c.lb = pick_lb(lcover, exchange == FF_XCHG_DSM ? 16 : num_sms);
-  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "plan's l cover cannot be split into ring members of <= 256 columns");
+  c.lb = pick_lb(lcover, exchange == FF_XCHG_DSM ? 16 : (exchange == FF_XCHG_L2_PAIR ? num_sms / 2 : num_sms));
+  if (!c.lb || (exchange == FF_XCHG_L2_PAIR && c.lb < 128))
+    return fail(FF_ERR_UNSUPPORTED, "plan's l cover cannot be split into ring members of <= 256 columns");
   c.ring = (int32_t)(lcover / c.lb);
   const int64_t ncover = (int64_t)cn * plan->block[1];  // cluster n cover (plan.py:236)
   const int64_t grid_n = ((plan->spatial_mask >> 1) & 1u) ? ch->n / ncover : 1;
   const int32_t reduce_sets = (cn * ck) / cl;
   c.n_splits = (int32_t)(grid_n * reduce_sets);
-  c.nb = gated ? 64 : 128;
+  c.nb = exchange == FF_XCHG_L2_PAIR ? (gated ? 128 : 256) : (gated ? 64 : 128);
   while (c.n_splits > 1 && ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.n_splits /= 2;
-  if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.nb = 64;
+  if (exchange != FF_XCHG_L2_PAIR && ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.nb = 64;
   if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb))
     return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");
   fill_machine(ch, &c, num_sms);

@@ -61,7 +61,16 @@ struct ChainArgs {
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
+  unsigned long long* prof;  // optional: per-CTA wait-cycle counters [grid][16] (diagnostics)
 };
+
+// Accumulate the cycles spent in `stmt` into `acc` when profiling is on.
+#define FF_TIMED(acc, stmt)                                           \
+  do {                                                                \
+    const unsigned long long _t0 = args.prof ? clock64() : 0ull;      \
+    stmt;                                                             \
+    if (args.prof) acc += clock64() - _t0;                            \
+  } while (0)
 
 __device__ __forceinline__ float apply_act(int act, float x) {
   switch (act) {
@@ -203,6 +212,8 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (elect_one()) {
+      unsigned long long w_empty = 0, w_flag = 0;
+      const unsigned long long t_start = clock64();
       int stage = 0, phase = 0;
       auto next = [&]() {
         if (++stage == kStages) {
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(256, 1)
         const Unit u = unit_of(T / steps);
         const int n0 = u.n0 + ((T % steps) * G + (int)p) * kNB;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(empty_bar(stage), phase ^ 1);
+          FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);
           tma_load_2d(sb, &tmA, full_bar(stage), kb * C::BK, u.m0);
@@ -239,13 +250,13 @@ __global__ void __launch_bounds__(256, 1)
           // wait until ring member `origin` published chunk (unit, t)
           const uint32_t* f = flag_addr(u, t, origin);
           uint32_t polls = 0;
-          while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
-          }
+          });
           fence_proxy_async_global();
         }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-          mbar_wait(empty_bar(stage), phase ^ 1);
+          FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), remote_c ? C::kG1_BYTES : C::kD_BYTES);
           if (remote_c) tma_load_2d(sb, &tmC, full_bar(stage), nrow0 + kb2 * C::BK, u.m0);
@@ -262,10 +273,18 @@ __global__ void __launch_bounds__(256, 1)
           load_hop(T, h);
         }
       }
+      if (args.prof) {
+        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        pr[0] = clock64() - t_start;
+        pr[1] = w_empty;
+        pr[2] = w_flag;
+      }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (elect_one()) {
+      unsigned long long w_full0 = 0, w_full1 = 0, w_cempty = 0, w_own = 0, w_eempty = 0;
+      const unsigned long long t_start = clock64();
       int stage = 0, phase = 0;
       auto next = [&]() {
         if (++stage == kStages) {
@@ -278,12 +297,12 @@ __global__ void __launch_bounds__(256, 1)
       auto gemm0 = [&](int T, int kb0, int kb1) {
         const int cb = T & 1;
         if (kb0 == 0) {
-          mbar_wait(c_empty[cb], ((T >> 1) & 1) ^ 1);
+          FF_TIMED(w_cempty, mbar_wait(c_empty[cb], ((T >> 1) & 1) ^ 1));
           tc_fence_after();
         }
         const uint32_t tacc = tmem_base + cb * C::kAcc;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(full_bar(stage), phase);
+          FF_TIMED(w_full0, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
 #pragma unroll
@@ -313,7 +332,7 @@ __global__ void __launch_bounds__(256, 1)
           // new unit: the epilogue must have drained the previous unit's E tile
           const int ui = T / steps;
           if (ui > 0) {
-            mbar_wait(e_empty, (ui - 1) & 1);
+            FF_TIMED(w_eempty, mbar_wait(e_empty, (ui - 1) & 1));
             tc_fence_after();
           }
           e_started = false;
@@ -321,7 +340,7 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t slot = 0;
         int b = 0;
         if (h == 0) {
-          mbar_wait(own_full, T & 1);
+          FF_TIMED(w_own, mbar_wait(own_full, T & 1));
           slot = own_slot;
         } else if (kDSM) {
           b = ri & 1;
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const bool from_stage = !kDSM && h > 0;
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-          mbar_wait(full_bar(stage), phase);
+          FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t ab = from_stage ? sb : slot + kb2 * (C::BM * C::BK * 2);
@@ -359,6 +378,15 @@ __global__ void __launch_bounds__(256, 1)
           if (T + 1 < total_steps) gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
           hop(T, h);
         }
+      }
+      if (args.prof) {
+        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        pr[3] = clock64() - t_start;
+        pr[4] = w_full0;
+        pr[5] = w_full1;
+        pr[6] = w_cempty;
+        pr[7] = w_own;
+        pr[8] = w_eempty;
       }
     }
   } else if (warp == 2) {
@@ -409,13 +437,15 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;  // TMEM lane quadrant
     const int row = q * 32 + (int)lane_id();
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    unsigned long long w_cfull = 0, w_ofree = 0, t_e = 0;
+    const unsigned long long t_start = clock64();
     for (int T = 0; T < total_steps; ++T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
       const int cb = T & 1;
-      mbar_wait(c_full[cb], (T >> 1) & 1);
+      FF_TIMED(w_cfull, mbar_wait(c_full[cb], (T >> 1) & 1));
       tc_fence_after();
-      mbar_wait(own_free, (T & 1) ^ 1);
+      FF_TIMED(w_ofree, mbar_wait(own_free, (T & 1) ^ 1));
       const uint32_t tacc = lane_base + cb * C::kAcc;
 #pragma unroll 1
       for (int c0 = 0; c0 < C::kCW; c0 += 16) {
@@ -466,6 +496,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (t == steps - 1) {
         // E tile of this unit: TMEM -> registers -> global
+        const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait(e_full, (T / steps) & 1);
         tc_fence_after();
         const int grow = u.m0 + row;
@@ -490,7 +521,15 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
         mbar_arrive(e_empty);
+        if (args.prof) t_e += clock64() - t_e0;
       }
+    }
+    if (args.prof && warp == 4 && lane_id() == 0) {
+      unsigned long long* pr = args.prof + blockIdx.x * 16;
+      pr[9] = clock64() - t_start;
+      pr[10] = w_cfull;
+      pr[11] = w_ofree;
+      pr[14] = t_e;
     }
   }
 

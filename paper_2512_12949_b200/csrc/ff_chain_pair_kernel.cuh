@@ -1,0 +1,408 @@
+// Fused GEMM-chain kernel, CTA-pair variant (tcgen05 cta_group::2).
+//
+// Same dataflow as ff_chain_kernel.cuh (ring of G members sharing the
+// intermediate C of an M tile, E slices accumulated in TMEM, GEMM1 hops of
+// n-step t interleaved with GEMM0 k-blocks of n-step t+1, L2-staged shuffle),
+// but every ring member is a CTA PAIR (a 2-CTA cluster) issuing M=256 MMAs:
+//   * CTA q of the pair owns rows [q*128, q*128+128) of the 256-row M tile
+//     (its A rows, its TMEM lanes, its C rows);
+//   * the weight operands are split by columns across the pair: CTA q loads
+//     half of each B / B0 / B1 / D tile, so each weight byte reaches one SM of
+//     the pair -- half the per-SM operand traffic of the single-CTA kernel;
+//   * the leader (cluster rank 0) issues all MMAs; both producers' TMA loads
+//     signal the leader's full barrier; commits multicast to both CTAs.
+// TMEM per CTA: C accumulator (256 columns; gated: two 128-column branch
+// accumulators) + E slice (kLB columns) = 512.
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader) + TMEM
+// alloc, w2/w3 idle, w4..w7 epilogue.
+#pragma once
+#include "ff_chain_kernel.cuh"
+
+namespace ff {
+
+template <bool kGated, int kLB, int kStages>
+struct PairCfg {
+  static constexpr int BM = 128;                   // rows per CTA (256 per pair)
+  static constexpr int BK = 64;
+  static constexpr int kN0 = kGated ? 128 : 256;   // C columns per pair per n-step (per branch if gated)
+  static constexpr int kCW = kN0;                  // C chunk width
+  static constexpr int kA_BYTES = BM * BK * 2;     // 16 KB
+  static constexpr int kBH = kN0 / 2;              // B columns held by one CTA (per branch)
+  static constexpr int kB_BYTES = (kGated ? 2 : 1) * BK * kBH * 2;  // 16 KB
+  static constexpr int kDH = kLB / 2;              // D columns held by one CTA
+  static constexpr int kD_BYTES = BK * kDH * 2;
+  static constexpr int kG0_BYTES = kA_BYTES + kB_BYTES;
+  static constexpr int kG1_BYTES = kA_BYTES + kD_BYTES;
+  static constexpr int kSTAGE = kG0_BYTES > kG1_BYTES ? kG0_BYTES : kG1_BYTES;
+  static constexpr int kCHUNK_BYTES = BM * kCW * 2;
+  static constexpr int kOFF_OWN = kStages * kSTAGE;
+  static constexpr int kOFF_BAR = kOFF_OWN + kCHUNK_BYTES;
+  static constexpr int kNUM_BARS = 2 * kStages + 8;
+  static constexpr int kSMEM = kOFF_BAR + kNUM_BARS * 8 + 16 + 1024;
+  static constexpr int kTMEM_E = 256;
+  static_assert(256 + kLB <= 512, "TMEM budget");
+  static_assert(kLB % 128 == 0 && kLB <= 256, "E slice: 128 or 256 columns");
+  static_assert(kSTAGE % 1024 == 0 && kCHUNK_BYTES % 1024 == 0, "SW128 alignment");
+};
+
+template <bool kGated, int kLB, int kStages>
+__global__ void __launch_bounds__(256, 1)
+    ff_chain_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                         const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
+                         const __grid_constant__ CUtensorMap tmC, const ChainArgs args) {
+  using C = PairCfg<kGated, kLB, kStages>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t base = (raw_base + 1023u) & ~1023u;
+  uint8_t* const smem_gen = smem_raw + (base - raw_base);
+
+  const int warp = threadIdx.x / 32;
+  const int G = args.G;                         // ring members (pairs)
+  const uint32_t q = cluster_rank();            // half of the pair (0 = leader)
+  const bool leader = (q == 0);
+  const int pair = blockIdx.x / 2;
+  const int p = pair % G;                       // ring position
+  const int ring = pair / G;
+  const int kblocks = args.K / C::BK;
+  const int steps = args.steps;
+  const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
+  const int total_steps = my_units * steps;
+
+  struct Unit {
+    int m0, l0, n0, id;
+  };
+  auto unit_of = [&](int i) {
+    const int u = ring + i * args.n_rings;
+    const int mt = u % args.m_tiles;
+    const int rest = u / args.m_tiles;
+    const int lc = rest % args.l_clusters;
+    const int split = rest / args.l_clusters;
+    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * steps * G * C::kN0, u};
+  };
+
+  const uint32_t bar0 = base + C::kOFF_BAR;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
+  const uint32_t bx = bar0 + 8u * (2 * kStages);
+  const uint32_t c_full = bx, c_empty = bx + 8, own_full = bx + 16, own_free = bx + 24;
+  const uint32_t e_full = bx + 32, e_empty = bx + 40;
+  const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
+  const uint32_t own_slot = base + C::kOFF_OWN;
+  constexpr uint16_t kPairMask = 0x3;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full_bar(s), 2);  // leader arrive.expect_tx + peer arrive
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(c_full, 1);
+    mbar_init(c_empty, 256);   // both CTAs' epilogues (leader's barrier is the one used)
+    mbar_init(own_full, 256);
+    mbar_init(own_free, G > 1 ? 2 : 1);
+    mbar_init(e_full, 1);
+    mbar_init(e_empty, 256);
+    fence_mbar_init();
+  }
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB0);
+    if (kGated) tma_prefetch_desc(&tmB1);
+    tma_prefetch_desc(&tmD);
+    if (G > 1) tma_prefetch_desc(&tmC);
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+
+  auto slot_lo = [&](int h) { return h * kblocks / G; };
+  auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
+    return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
+  };
+  // leader-side addresses of pair-shared barriers
+  const uint32_t L_c_empty = mapa(c_empty, 0), L_own_full = mapa(own_full, 0), L_e_empty = mapa(e_empty, 0);
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (elect_one()) {
+      unsigned long long w_empty = 0, w_flag = 0;
+      const unsigned long long t_start = clock64();
+      int stage = 0, phase = 0;
+      auto next = [&]() {
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      auto arm = [&](int bytes) {
+        if (leader)
+          mbar_expect_tx(full_bar(stage), 2 * bytes);
+        else
+          mbar_arrive_remote(mapa(full_bar(stage), 0));
+      };
+      auto load_gemm0 = [&](int T, int kb0, int kb1) {
+        const Unit u = unit_of(T / steps);
+        const int n0 = u.n0 + ((T % steps) * G + p) * C::kN0 + (int)q * C::kBH;  // this CTA's B columns
+        for (int kb = kb0; kb < kb1; ++kb) {
+          FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
+          const uint32_t sb = base + stage * C::kSTAGE;
+          const uint32_t lb = mapa(full_bar(stage), 0);
+          arm(C::kG0_BYTES);
+          tma_load_2d_pair(sb, &tmA, lb, kb * C::BK, u.m0 + (int)q * C::BM);
+          if (kGated) {
+            tma_load_2d_pair(sb + C::kA_BYTES, &tmB0, lb, n0, kb * C::BK);
+            tma_load_2d_pair(sb + C::kA_BYTES + C::BK * C::kBH * 2, &tmB1, lb, n0, kb * C::BK);
+          } else {
+#pragma unroll
+            for (int j = 0; j < C::kBH / 64; ++j)
+              tma_load_2d_pair(sb + C::kA_BYTES + j * 8192, &tmB0, lb, n0 + 64 * j, kb * C::BK);
+          }
+          next();
+        }
+      };
+      auto load_hop = [&](int T, int h) {
+        const Unit u = unit_of(T / steps);
+        const int t = T % steps;
+        const int origin = (p - h + G) % G;
+        const int nrow0 = u.n0 + (t * G + origin) * C::kN0;
+        const bool remote_c = h > 0;
+        if (remote_c) {
+          const uint32_t* f = flag_addr(u, t, origin, (int)q);
+          uint32_t polls = 0;
+          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+          });
+          fence_proxy_async_global();
+        }
+        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+          FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
+          const uint32_t sb = base + stage * C::kSTAGE;
+          const uint32_t lb = mapa(full_bar(stage), 0);
+          arm(remote_c ? C::kG1_BYTES : C::kD_BYTES);
+          if (remote_c) tma_load_2d_pair(sb, &tmC, lb, nrow0 + kb2 * C::BK, u.m0 + (int)q * C::BM);
+#pragma unroll
+          for (int j = 0; j < C::kDH / 64; ++j)
+            tma_load_2d_pair(sb + C::kA_BYTES + j * 8192, &tmD, lb, u.l0 + (int)q * C::kDH + 64 * j,
+                             nrow0 + kb2 * C::BK);
+          next();
+        }
+      };
+      if (total_steps > 0) load_gemm0(0, 0, kblocks);
+      for (int T = 0; T < total_steps; ++T) {
+        for (int h = 0; h < G; ++h) {
+          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          load_hop(T, h);
+        }
+      }
+      if (args.prof) {
+        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        pr[0] = clock64() - t_start;
+        pr[1] = w_empty;
+        pr[2] = w_flag;
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (leader && elect_one()) {
+      unsigned long long w_full0 = 0, w_full1 = 0, w_cempty = 0, w_own = 0, w_eempty = 0;
+      const unsigned long long t_start = clock64();
+      int stage = 0, phase = 0;
+      auto next = [&]() {
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      };
+      constexpr uint32_t idesc0 = idesc_bf16(256, C::kN0, 0, 1);
+      constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
+      auto gemm0 = [&](int T, int kb0, int kb1) {
+        if (kb0 == 0) {
+          FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, (T & 1) ^ 1));
+          tc_fence_after();
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
+          FF_TIMED(w_full0, mbar_wait(full_bar(stage), phase));
+          tc_fence_after();
+          const uint32_t sb = base + stage * C::kSTAGE;
+#pragma unroll
+          for (int kk = 0; kk < C::BK / 16; ++kk) {
+            const uint64_t ad = desc_kmajor_sw128(sb + kk * 32);
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            if (kGated) {
+              const uint64_t b0 = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
+              const uint64_t b1 = desc_mnmajor_sw128(sb + C::kA_BYTES + C::BK * C::kBH * 2 + kk * 2048, 8192);
+              umma_bf16_pair(tmem_base, ad, b0, idesc0, acc);
+              umma_bf16_pair(tmem_base + C::kN0, ad, b1, idesc0, acc);
+            } else {
+              const uint64_t bd = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
+              umma_bf16_pair(tmem_base, ad, bd, idesc0, acc);
+            }
+          }
+          umma_commit_pair(empty_bar(stage), kPairMask);
+          next();
+        }
+        if (kb1 == kblocks) umma_commit_pair(c_full, kPairMask);
+      };
+      bool e_started = false;
+      auto hop = [&](int T, int h) {
+        const int t = T % steps;
+        if (t == 0 && h == 0) {
+          const int ui = T / steps;
+          if (ui > 0) {
+            FF_TIMED(w_eempty, mbar_wait_cluster(e_empty, (ui - 1) & 1));
+            tc_fence_after();
+          }
+          e_started = false;
+        }
+        if (h == 0) FF_TIMED(w_own, mbar_wait_cluster(own_full, T & 1));
+        tc_fence_after();
+        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+          FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
+          tc_fence_after();
+          const uint32_t sb = base + stage * C::kSTAGE;
+          const uint32_t ab = (h == 0) ? own_slot + kb2 * (C::BM * C::BK * 2) : sb;
+#pragma unroll
+          for (int kk = 0; kk < C::BK / 16; ++kk) {
+            const uint64_t ad = desc_kmajor_sw128(ab + kk * 32);
+            const uint64_t bd = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
+            umma_bf16_pair(tmem_base + C::kTMEM_E, ad, bd, idesc1, e_started ? 1u : 0u);
+            e_started = true;
+          }
+          umma_commit_pair(empty_bar(stage), kPairMask);
+          next();
+        }
+        if (h == 0) umma_commit_pair(own_free, kPairMask);
+        if (t == steps - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
+      };
+      if (total_steps > 0) gemm0(0, 0, kblocks);
+      for (int T = 0; T < total_steps; ++T) {
+        for (int h = 0; h < G; ++h) {
+          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          hop(T, h);
+        }
+      }
+      if (args.prof) {
+        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        pr[3] = clock64() - t_start;
+        pr[4] = w_full0;
+        pr[5] = w_full1;
+        pr[6] = w_cempty;
+        pr[7] = w_own;
+        pr[8] = w_eempty;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue (both CTAs) =====================
+    const int wq = warp & 3;
+    const int row = wq * 32 + (int)lane_id();
+    const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
+    unsigned long long w_cfull = 0, w_ofree = 0, t_drain = 0, t_store = 0, t_e = 0;
+    const unsigned long long t_start = clock64();
+    for (int T = 0; T < total_steps; ++T) {
+      const Unit u = unit_of(T / steps);
+      const int t = T % steps;
+      FF_TIMED(w_cfull, mbar_wait_cluster(c_full, T & 1));
+      tc_fence_after();
+      FF_TIMED(w_ofree, mbar_wait_cluster(own_free, (T & 1) ^ 1));
+      const unsigned long long t_d0 = args.prof ? clock64() : 0ull;
+#pragma unroll 1
+      for (int c0 = 0; c0 < C::kCW; c0 += 32) {
+        float v[32];
+        tmem_ld32(lane_base + c0, v);
+        if (kGated) {
+          float w[32];
+          tmem_ld32(lane_base + C::kN0 + c0, w);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = (v[i] / (1.0f + __expf(-v[i]))) * w[i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = apply_act(args.act, v[i]);
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        const int sub = c0 / 64;
+        const int ch = (c0 % 64) / 8;
+        const uint32_t rowb = own_slot + sub * (C::BM * C::BK * 2) + row * 128;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_shared_v4(rowb + (((ch + j) ^ (row & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        const int grow = u.m0 + (int)q * C::BM + row;
+        if (args.c_debug != nullptr && grow < args.M) {
+          const int ncol = u.n0 + (t * G + p) * C::kN0 + c0;
+          uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)grow * args.N + ncol);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_remote(L_c_empty);
+      fence_proxy_async_smem();
+      mbar_arrive_remote(L_own_full);
+      if (args.prof) t_drain += clock64() - t_d0;
+      const unsigned long long t_s0 = args.prof ? clock64() : 0ull;
+      if (G > 1) {
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane_id() == 0) {
+          const int ncol = u.n0 + (t * G + p) * C::kN0;
+#pragma unroll
+          for (int sub = 0; sub < C::kCW / 64; ++sub)
+            tma_store_2d(&tmC, own_slot + sub * (C::BM * C::BK * 2), ncol + 64 * sub, u.m0 + (int)q * C::BM);
+          bulk_commit();
+          bulk_wait0();
+          fence_proxy_async_global();
+          st_release_gpu_u32(flag_addr(u, t, p, (int)q), args.epoch);
+          mbar_arrive(own_free);
+        }
+      }
+      if (args.prof) t_store += clock64() - t_s0;
+      if (t == steps - 1) {
+        const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
+        mbar_wait_cluster(e_full, (T / steps) & 1);
+        tc_fence_after();
+        const int grow = u.m0 + (int)q * C::BM + row;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kLB; c0 += 32) {
+          float v[32];
+          tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+          if (grow < args.M) {
+            if (args.S == 1) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              uint4* dst = reinterpret_cast<uint4*>(args.E + (size_t)grow * args.L + u.l0 + c0);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            } else {
+              float* dst = args.ws + (size_t)grow * args.L + u.l0 + c0;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) red_add_v4_f32(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_remote(L_e_empty);
+        if (args.prof) t_e += clock64() - t_e0;
+      }
+    }
+    if (args.prof && warp == 4 && lane_id() == 0) {
+      unsigned long long* pr = args.prof + blockIdx.x * 16;
+      pr[9] = clock64() - t_start;
+      pr[10] = w_cfull;
+      pr[11] = w_ofree;
+      pr[12] = t_drain;
+      pr[13] = t_store;
+      pr[14] = t_e;
+    }
+  }
+
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair<512>(tmem_base);
+  }
+}
+
+}  // namespace ff

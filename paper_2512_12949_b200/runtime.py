@@ -44,7 +44,7 @@ def _num_sms() -> int:
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
-EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2}
+EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2, "pair": nat.XCHG_L2_PAIR}
 
 
 def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None,

@@ -47,7 +47,17 @@ cases=[(128,128,64,64,0,False,(1,1,128,64)),(128,256,128,256,1,False,(1,1,128,25
        (256,1024,512,512,2,True,(2,1,64,256)),(128,3072,128,2048,1,False,(8,1,128,256)),(128,1536,256,1024,1,False,(4,1,64,256)),
        (3136,64,576,256,1,False,None),(512,3072,768,768,3,False,None),(512,8192,2048,2048,2,True,None),(512,16384,4096,4096,1,False,None),
        (1024,8192,2048,2048,1,False,None)]
-for xchg in (1,0):
+pair_cases=[(256,256,128,256,1,False,(1,1,256,256)),(256,512,128,512,1,False,(2,1,256,256)),(512,1024,256,1024,1,False,(4,1,256,256)),
+            (512,1024,256,1024,1,False,(4,2,256,256)),(256,512,256,256,2,True,(1,1,128,256)),(256,1024,256,512,2,True,(2,2,128,256)),
+            (200,1536,256,768,3,False,(3,2,256,256)),(512,1024,256,512,1,False,(4,1,256,128)),
+            (3136,512,576,256,1,False,None),(512,3072,768,768,3,False,None),(512,8192,2048,2048,2,True,None),(512,16384,4096,4096,1,False,None),
+            (1024,8192,2048,2048,1,False,None)]
+for c in pair_cases:
+    try:
+        run(*c, xchg=2)
+    except Exception as e:
+        print("FAIL", 2, c, repr(e), flush=True)
+for xchg in ([] if len(sys.argv) > 1 else (1,0)):
     for c in cases:
         try:
             run(*c, xchg=xchg)
@@ -65,7 +75,7 @@ def bench(m,n,k,l,g,act,xchg,cfg=None,iters=20):
     return ms, fl, kc
 for (m,n,k,l,act,g) in [(512,16384,4096,4096,1,False),(512,8192,2048,2048,2,True),(512,3072,768,768,3,False),(4096,8192,2048,2048,1,False),(3136,64,576,256,1,False)]:
     line=f"TIME m{m} n{n} k{k} l{l} g{int(g)}:"
-    for xchg in (1,0):
+    for xchg in (2,1,0):
         try:
             ms,fl,kc=bench(m,n,k,l,g,act,xchg)
             line+=f" | x{xchg} {ms*1e3:.1f}us {fl/ms/1e9:.0f}TF/s r{kc.ring} s{kc.n_splits} rings{kc.rings}"
