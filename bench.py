@@ -210,7 +210,10 @@ def make_device_inputs(kind, m, n, k, l, seed, device):
         return (torch.rand(*shape, generator=g) * 2 - 1).to(torch.bfloat16).to(device)
     t = {"A": u(m, k), "D": u(n, l)}
     if kind == "gated_ffn":
-        t["B0"], t["B1"] = u(k, n), u(k, n)
+        # gate|up weights stored as one packed [2][K][N] tensor (the fused gate_up_proj
+        # layout): one TMA box fetches both branches
+        w = u(2, k, n)
+        t["B0"], t["B1"] = w[0], w[1]
     else:
         t["B"] = u(k, n)
     return t
@@ -235,11 +238,16 @@ def choose_config(name, tensors):
     cands = []
     entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
     plans = [plan_from_dict(p) for p in entry["top"]] if entry else []
-    timed = runtime.profile_best_from_list(graph, plans, tensors, iters=5, warmup=2) if plans else []
-    cands += [(ms, cfg, plan.describe()) for ms, plan, cfg in timed]
-    auto = runtime.lower(graph, None)
-    ms_auto = runtime.profile_configs(graph, [auto], tensors, iters=5, warmup=2)[0][0]
-    cands.append((ms_auto, auto, "runtime-auto"))
+    timed = runtime.profile_best_from_list(graph, plans, tensors, iters=5, warmup=2,
+                                           exchanges=("pair", "l2", "dsm")) if plans else []
+    cands += [(ms, cfg, f"{plan.describe()} [{runtime.exchange_name(cfg)}]") for ms, plan, cfg in timed]
+    for exchange in ("pair", "l2", "dsm"):
+        try:
+            auto = runtime.lower(graph, None, exchange=exchange)
+        except Exception:
+            continue
+        ms_auto = runtime.profile_configs(graph, [auto], tensors, iters=5, warmup=2)[0][0]
+        cands.append((ms_auto, auto, f"runtime-auto [{exchange}]"))
     cands.sort(key=lambda c: c[0])
     return cands[0][1], cands[0][2], [(round(c[0] * 1e3, 2), c[2]) for c in cands]
 

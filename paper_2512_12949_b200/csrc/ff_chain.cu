@@ -59,6 +59,24 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
   return r == CUDA_SUCCESS;
 }
 
+// Generic N-D map (dims innermost first; strides in bytes for dims 1..rank-1).
+bool make_map_nd(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
+                 const uint64_t* strides, const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  return fn(map, dt, rank, const_cast<void*>(ptr), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 int num_sms_cached() {
   static int n = -1;
   if (n < 0) {
@@ -100,19 +118,20 @@ struct WsLayout {
   size_t e_off, c_off, f_off, total;
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+// Workspace: [flags, fixed 1 MiB at offset 0 in EVERY layout][fp32 E][C scratch].
+// The flags region never holds anything but epoch stamps, whatever config
+// used the workspace before, so a stale stamp is always older than the
+// current launch's epoch.
+constexpr size_t kFlagBytes = 1u << 20;
 WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   WsLayout w{};
-  size_t off = 0;
+  const bool pair = c->exchange == FF_XCHG_L2_PAIR;
+  w.f_off = 0;
+  size_t off = kFlagBytes;
   w.e_off = off;
   if (c->n_splits > 1) off = align256(off + (size_t)ch->m * ch->l * sizeof(float));
-  const bool pair = c->exchange == FF_XCHG_L2_PAIR;
   w.c_off = off;
-  if (c->exchange != FF_XCHG_DSM && c->ring > 1) {
-    off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
-  }
-  w.f_off = off;
-  if (c->exchange != FF_XCHG_DSM)
-    off = align256(off + (size_t)c->units * c->steps * c->ring * (pair ? 2 : 1) * sizeof(uint32_t));
+  if (c->exchange != FF_XCHG_DSM && c->ring > 1) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   w.total = off;
   return w;
 }
@@ -215,21 +234,21 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   return FF_OK;
 }
 
-template <bool kGated, int kLB>
+template <bool kGated>
 struct PairStages {
-  using Probe = ff::PairCfg<kGated, kLB, 1>;
+  using Probe = ff::PairCfg<kGated, 256, 1>;
   static constexpr int kFixed = Probe::kSMEM - Probe::kSTAGE - 2 * 8;
   static constexpr int kMax = (232448 - kFixed - 64) / (Probe::kSTAGE + 16);
-  static constexpr int value = kMax > 8 ? 8 : kMax;
+  static constexpr int value = kMax > 4 ? 4 : kMax;
 };
 
-template <bool kGated, int kLB>
+template <bool kGated, bool kPacked>
 int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
                      cudaStream_t stream) {
-  constexpr int kStages = PairStages<kGated, kLB>::value;
-  static_assert(kStages >= 3, "not enough shared memory for a pipeline");
-  using C = ff::PairCfg<kGated, kLB, kStages>;
-  auto kern = ff::ff_chain_pair_kernel<kGated, kLB, kStages>;
+  constexpr int kStages = PairStages<kGated>::value;
+  static_assert(kStages >= 2, "not enough shared memory for a pipeline");
+  using C = ff::PairCfg<kGated, 256, kStages>;
+  auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM); });
@@ -239,14 +258,48 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   const uint64_t M = ch->m, N = ch->n, K = ch->k, L = ch->l;
   const WsLayout wl = ws_layout(ch, cfg);
   uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
-  CUtensorMap mA, mB0, mB1, mD, mC;
-  bool ok = make_map(&mA, t->a, M, K, 64, 128);
-  ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
-  ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
-  ok = ok && make_map(&mD, t->d, N, L, 64, 64);
-  const bool l2x = cfg->ring > 1;
-  ok = ok && make_map(&mC, l2x ? (const void*)(wsb + wl.c_off) : t->a, l2x ? (uint64_t)cfg->m_tiles * 256 : M,
-                      l2x ? N : K, 64, 128);
+  const uint64_t mpad = (uint64_t)cfg->m_tiles * 256;
+  ff::PairMaps maps;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  bool ok = true;
+  {  // A [M][K] as {64, M, K/64}
+    const uint64_t d[3] = {64, M, K / 64}, st[2] = {K * 2, 128};
+    const uint32_t b[3] = {64, 128, 2};
+    ok = ok && make_map_nd(&maps.a, BF, 3, t->a, d, st, b);
+  }
+  if (kGated && kPacked) {  // packed [2][K][N] as {64, K, N/64, 2}
+    const uint64_t d[4] = {64, K, N / 64, 2}, st[3] = {N * 2, 128, K * N * 2};
+    const uint32_t b[4] = {64, 128, 1, 2};
+    ok = ok && make_map_nd(&maps.b, BF, 4, t->b, d, st, b);
+    maps.b1 = maps.b;
+  } else {
+    const uint64_t d[3] = {64, K, N / 64}, st[2] = {N * 2, 128};
+    const uint32_t b[3] = {64, 128, kGated ? 1u : 2u};
+    ok = ok && make_map_nd(&maps.b, BF, 3, t->b, d, st, b);
+    ok = ok && make_map_nd(&maps.b1, BF, 3, kGated ? t->b1 : t->b, d, st, b);
+  }
+  {  // D [N][L] as {64, N, L/64}
+    const uint64_t d[3] = {64, N, L / 64}, st[2] = {L * 2, 128};
+    const uint32_t b[3] = {64, 128, 2};
+    ok = ok && make_map_nd(&maps.d, BF, 3, t->d, d, st, b);
+  }
+  {  // C scratch [mpad][N] as {64, mpad, N/64}
+    const bool l2x = cfg->ring > 1;
+    const uint64_t d[3] = {64, l2x ? mpad : M, l2x ? N / 64 : K / 64}, st[2] = {(l2x ? N : K) * 2, 128};
+    const uint32_t b[3] = {64, 128, 2};
+    ok = ok && make_map_nd(&maps.c, BF, 3, l2x ? (const void*)(wsb + wl.c_off) : t->a, d, st, b);
+  }
+  {  // E [M][L] bf16, box {64, 128}
+    const uint64_t d[2] = {L, M}, st[1] = {L * 2};
+    const uint32_t b[2] = {64, 128};
+    ok = ok && make_map_nd(&maps.e, BF, 2, t->e, d, st, b);
+  }
+  {  // fp32 workspace [M][L], box {32, 128}
+    const uint64_t d[2] = {L, M}, st[1] = {L * 4};
+    const uint32_t b[2] = {32, 128};
+    ok = ok && make_map_nd(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, cfg->n_splits > 1 ? (const void*)(wsb + wl.e_off) : t->e,
+                           d, st, b);
+  }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   const int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
@@ -288,12 +341,12 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   attr[1].val.cooperative = 1;
   lc.attrs = attr;
   lc.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, a);
   if (e != cudaSuccess) {
     // cooperative + cluster not accepted: the grid is sized to co-residency anyway
     cudaGetLastError();
     lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
+    e = cudaLaunchKernelEx(&lc, kern, maps, a);
   }
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx(pair): ") + cudaGetErrorString(e));
   if (cfg->n_splits > 1) {
@@ -304,16 +357,22 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   return FF_OK;
 }
 
+int launch_pair_dispatch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
+                         void* c_debug, cudaStream_t stream) {
+  if (ch->kind != FF_KIND_GATED) return launch_pair_impl<false, false>(ch, cfg, t, ws, c_debug, stream);
+  // gate|up packed as one [2][K][N] tensor: one TMA box fetches both branches
+  const bool packed = reinterpret_cast<const uint8_t*>(t->b1) ==
+                      reinterpret_cast<const uint8_t*>(t->b) + (size_t)ch->k * ch->n * 2;
+  return packed ? launch_pair_impl<true, true>(ch, cfg, t, ws, c_debug, stream)
+                : launch_pair_impl<true, false>(ch, cfg, t, ws, c_debug, stream);
+}
+
 using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);
 
 LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
   if (mode == FF_XCHG_L2_PAIR) {
-    if (nb != (gated ? 128 : 256)) return nullptr;
-    if (gated && lb == 256) return &launch_pair_impl<true, 256>;
-    if (gated && lb == 128) return &launch_pair_impl<true, 128>;
-    if (!gated && lb == 256) return &launch_pair_impl<false, 256>;
-    if (!gated && lb == 128) return &launch_pair_impl<false, 128>;
-    return nullptr;
+    if (nb != (gated ? 128 : 256) || lb != 256) return nullptr;
+    return &launch_pair_dispatch;
   }
 #define FF_CASE(G, NB, LB)                                                    \
   if (gated == G && nb == NB && lb == LB)                                     \
@@ -356,6 +415,8 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
     return fail(FF_ERR_UNSUPPORTED, "ring size out of range (DSM rings are clusters of <= 16 CTAs)");
   if (c->n_splits < 1) return fail(FF_ERR_UNSUPPORTED, "n_splits must be >= 1");
   if (!select_kernel(gated, c->nb, c->lb, c->exchange)) return fail(FF_ERR_UNSUPPORTED, "no kernel for (nb, lb)");
+  if (c->exchange == FF_XCHG_L2_PAIR && (ch->k % 128 || c->lb != 256))
+    return fail(FF_ERR_UNSUPPORTED, "pair kernel needs k % 128 == 0 and 256-column E slices");
   const int64_t lcover = (int64_t)c->ring * c->lb;
   if (ch->l % lcover) return fail(FF_ERR_UNSUPPORTED, "ring * lb must divide l");
   const int64_t nstep = (int64_t)c->n_splits * c->ring * c->nb;
@@ -519,6 +580,9 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   if (rc) return rc;
   const size_t need = ws_layout(ch, &cfg).total;
   if (need && (ws == nullptr || ws_bytes < need)) return fail(FF_ERR_ARG, "workspace too small");
+  if (cfg.exchange != FF_XCHG_DSM &&
+      (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes)
+    return fail(FF_ERR_UNSUPPORTED, "too many (unit, step, member) chunks for the flag region");
   if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(FF_ERR_ARG, "workspace must be 256-byte aligned");
   LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb, cfg.exchange);
   return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream));

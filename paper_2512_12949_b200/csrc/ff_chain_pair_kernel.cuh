@@ -1,18 +1,23 @@
 // Fused GEMM-chain kernel, CTA-pair variant (tcgen05 cta_group::2).
 //
-// Same dataflow as ff_chain_kernel.cuh (ring of G members sharing the
-// intermediate C of an M tile, E slices accumulated in TMEM, GEMM1 hops of
-// n-step t interleaved with GEMM0 k-blocks of n-step t+1, L2-staged shuffle),
-// but every ring member is a CTA PAIR (a 2-CTA cluster) issuing M=256 MMAs:
-//   * CTA q of the pair owns rows [q*128, q*128+128) of the 256-row M tile
-//     (its A rows, its TMEM lanes, its C rows);
-//   * the weight operands are split by columns across the pair: CTA q loads
-//     half of each B / B0 / B1 / D tile, so each weight byte reaches one SM of
-//     the pair -- half the per-SM operand traffic of the single-CTA kernel;
-//   * the leader (cluster rank 0) issues all MMAs; both producers' TMA loads
+// Same dataflow as ff_chain_kernel.cuh -- a ring of G members shares the
+// intermediate C of an M tile, each member accumulates an E slice in TMEM,
+// GEMM1 hops of n-step t are interleaved with GEMM0 k-blocks of n-step t+1,
+// and C is exchanged through an L2-resident scratch -- but every ring member
+// is a CTA PAIR (a 2-CTA cluster) issuing M=256 MMAs:
+//   * CTA q of the pair owns rows [q*128, q*128+128) of the 256-row M tile;
+//   * weight operands are split by columns across the pair (CTA q loads half
+//     of every B / B0|B1 / D tile), so each weight byte reaches one SM;
+//   * the leader (cluster rank 0) issues the MMAs; both producers' TMA loads
 //     signal the leader's full barrier; commits multicast to both CTAs.
+// TMA shape rule (measured, profiles/r01/tma_stream.log): the TMA unit costs
+// ~0.3-0.5 us per instruction regardless of size, so every operand tile is a
+// single 32 KB 3D/4D box: k-blocks are 128 deep (stage = 2 x 32 KB), the gated
+// branches are fetched by one 4D box from a packed [2][K][N] gate|up weight,
+// and the E tile leaves through TMA stores (S == 1) or TMA fp32 reduce-adds
+// (S > 1, inter-cluster reduce) staged in shared memory.
 // TMEM per CTA: C accumulator (256 columns; gated: two 128-column branch
-// accumulators) + E slice (kLB columns) = 512.
+// accumulators) + E slice (kLB columns).
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader) + TMEM
 // alloc, w2/w3 idle, w4..w7 epilogue.
 #pragma once
@@ -20,36 +25,37 @@
 
 namespace ff {
 
+struct PairMaps {
+  CUtensorMap a;    // A [M][K]: 3D {64, M, K/64}, box {64, 128, 2}
+  CUtensorMap b;    // std: B [K][N] 3D {64, K, N/64} box {64, 128, 2}; gated packed: [2][K][N] 4D box {64,128,1,2}
+  CUtensorMap b1;   // gated, unpacked: B1 (3D, box {64, 128, 1}); b is then B0 with the same box
+  CUtensorMap d;    // D [N][L]: 3D {64, N, L/64}, box {64, 128, 2}
+  CUtensorMap c;    // C scratch [Mpad][N]: 3D {64, Mpad, N/64}, box {64, 128, 2}
+  CUtensorMap e;    // E [M][L] bf16: 2D box {64, 128}
+  CUtensorMap w;    // fp32 workspace [M][L]: 2D box {32, 128}
+};
+
 template <bool kGated, int kLB, int kStages>
 struct PairCfg {
-  static constexpr int BM = 128;                   // rows per CTA (256 per pair)
-  static constexpr int BK = 64;
-  static constexpr int kN0 = kGated ? 128 : 256;   // C columns per pair per n-step (per branch if gated)
-  static constexpr int kCW = kN0;                  // C chunk width
-  static constexpr int kA_BYTES = BM * BK * 2;     // 16 KB
-  static constexpr int kBH = kN0 / 2;              // B columns held by one CTA (per branch)
-  static constexpr int kB_BYTES = (kGated ? 2 : 1) * BK * kBH * 2;  // 16 KB
-  static constexpr int kDH = kLB / 2;              // D columns held by one CTA
-  static constexpr int kD_BYTES = BK * kDH * 2;
-  static constexpr int kG0_BYTES = kA_BYTES + kB_BYTES;
-  static constexpr int kG1_BYTES = kA_BYTES + kD_BYTES;
-  static constexpr int kSTAGE = kG0_BYTES > kG1_BYTES ? kG0_BYTES : kG1_BYTES;
-  static constexpr int kCHUNK_BYTES = BM * kCW * 2;
+  static constexpr int BM = 128;                  // rows per CTA (256 per pair)
+  static constexpr int BK = 128;                  // k depth of one stage
+  static constexpr int kN0 = kGated ? 128 : 256;  // C columns per pair per n-step
+  static constexpr int kCW = kN0;
+  static constexpr int kSLOT = 32768;             // one operand tile (A or B / C or D) per stage
+  static constexpr int kSTAGE = 2 * kSLOT;
+  static constexpr int kCHUNK_BYTES = BM * kCW * 2;  // own C chunk (bf16, K-major SW128 64-col tiles)
   static constexpr int kOFF_OWN = kStages * kSTAGE;
   static constexpr int kOFF_BAR = kOFF_OWN + kCHUNK_BYTES;
   static constexpr int kNUM_BARS = 2 * kStages + 8;
   static constexpr int kSMEM = kOFF_BAR + kNUM_BARS * 8 + 16 + 1024;
   static constexpr int kTMEM_E = 256;
   static_assert(256 + kLB <= 512, "TMEM budget");
-  static_assert(kLB % 128 == 0 && kLB <= 256, "E slice: 128 or 256 columns");
-  static_assert(kSTAGE % 1024 == 0 && kCHUNK_BYTES % 1024 == 0, "SW128 alignment");
+  static_assert(kLB == 256 || kLB == 128, "E slice: 128 or 256 columns");
 };
 
-template <bool kGated, int kLB, int kStages>
+template <bool kGated, int kLB, int kStages, bool kPackedB>
 __global__ void __launch_bounds__(256, 1)
-    ff_chain_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                         const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
-                         const __grid_constant__ CUtensorMap tmC, const ChainArgs args) {
+    ff_chain_pair_kernel(const __grid_constant__ PairMaps maps, const ChainArgs args) {
   using C = PairCfg<kGated, kLB, kStages>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_base = smem_u32(smem_raw);
@@ -57,11 +63,11 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
   const int warp = threadIdx.x / 32;
-  const int G = args.G;                         // ring members (pairs)
-  const uint32_t q = cluster_rank();            // half of the pair (0 = leader)
+  const int G = args.G;                  // ring members (pairs)
+  const uint32_t q = cluster_rank();     // half of the pair (0 = leader)
   const bool leader = (q == 0);
   const int pair = blockIdx.x / 2;
-  const int p = pair % G;                       // ring position
+  const int p = pair % G;                // ring position
   const int ring = pair / G;
   const int kblocks = args.K / C::BK;
   const int steps = args.steps;
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(c_full, 1);
-    mbar_init(c_empty, 256);   // both CTAs' epilogues (leader's barrier is the one used)
+    mbar_init(c_empty, 256);  // both CTAs' epilogues arrive on the leader's barrier
     mbar_init(own_full, 256);
     mbar_init(own_free, G > 1 ? 2 : 1);
     mbar_init(e_full, 1);
@@ -104,11 +110,11 @@ __global__ void __launch_bounds__(256, 1)
     fence_mbar_init();
   }
   if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB0);
-    if (kGated) tma_prefetch_desc(&tmB1);
-    tma_prefetch_desc(&tmD);
-    if (G > 1) tma_prefetch_desc(&tmC);
+    tma_prefetch_desc(&maps.a);
+    tma_prefetch_desc(&maps.b);
+    if (kGated && !kPackedB) tma_prefetch_desc(&maps.b1);
+    tma_prefetch_desc(&maps.d);
+    if (G > 1) tma_prefetch_desc(&maps.c);
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
   tc_fence_before();
@@ -120,7 +126,6 @@ __global__ void __launch_bounds__(256, 1)
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
   };
-  // leader-side addresses of pair-shared barriers
   const uint32_t L_c_empty = mapa(c_empty, 0), L_own_full = mapa(own_full, 0), L_e_empty = mapa(e_empty, 0);
 
   if (warp == 0) {
@@ -135,28 +140,29 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
-      auto arm = [&](int bytes) {
+      auto arm = [&]() {
         if (leader)
-          mbar_expect_tx(full_bar(stage), 2 * bytes);
+          mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
         else
           mbar_arrive_remote(mapa(full_bar(stage), 0));
       };
       auto load_gemm0 = [&](int T, int kb0, int kb1) {
         const Unit u = unit_of(T / steps);
-        const int n0 = u.n0 + ((T % steps) * G + p) * C::kN0 + (int)q * C::kBH;  // this CTA's B columns
+        // first 64-column block of this CTA's half of the chunk (gated: of each branch)
+        const int nblk = (u.n0 + ((T % steps) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
         for (int kb = kb0; kb < kb1; ++kb) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), 0);
-          arm(C::kG0_BYTES);
-          tma_load_2d_pair(sb, &tmA, lb, kb * C::BK, u.m0 + (int)q * C::BM);
-          if (kGated) {
-            tma_load_2d_pair(sb + C::kA_BYTES, &tmB0, lb, n0, kb * C::BK);
-            tma_load_2d_pair(sb + C::kA_BYTES + C::BK * C::kBH * 2, &tmB1, lb, n0, kb * C::BK);
+          arm();
+          tma_load_3d_pair(sb, &maps.a, lb, 0, u.m0 + (int)q * C::BM, kb * (C::BK / 64));
+          if (!kGated) {
+            tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
+          } else if (kPackedB) {
+            tma_load_4d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0);
           } else {
-#pragma unroll
-            for (int j = 0; j < C::kBH / 64; ++j)
-              tma_load_2d_pair(sb + C::kA_BYTES + j * 8192, &tmB0, lb, n0 + 64 * j, kb * C::BK);
+            tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
+            tma_load_3d_pair(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk);
           }
           next();
         }
@@ -165,9 +171,9 @@ __global__ void __launch_bounds__(256, 1)
         const Unit u = unit_of(T / steps);
         const int t = T % steps;
         const int origin = (p - h + G) % G;
-        const int nrow0 = u.n0 + (t * G + origin) * C::kN0;
-        const bool remote_c = h > 0;
-        if (remote_c) {
+        const int ncol0 = u.n0 + (t * G + origin) * C::kN0;
+        const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
+        if (h > 0) {
           const uint32_t* f = flag_addr(u, t, origin, (int)q);
           uint32_t polls = 0;
           FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
@@ -179,12 +185,12 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), 0);
-          arm(remote_c ? C::kG1_BYTES : C::kD_BYTES);
-          if (remote_c) tma_load_2d_pair(sb, &tmC, lb, nrow0 + kb2 * C::BK, u.m0 + (int)q * C::BM);
-#pragma unroll
-          for (int j = 0; j < C::kDH / 64; ++j)
-            tma_load_2d_pair(sb + C::kA_BYTES + j * 8192, &tmD, lb, u.l0 + (int)q * C::kDH + 64 * j,
-                             nrow0 + kb2 * C::BK);
+          if (leader)
+            mbar_expect_tx(full_bar(stage), 2 * (h > 0 ? C::kSTAGE : C::kSLOT));
+          else
+            mbar_arrive_remote(lb);
+          if (h > 0) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
+          tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
           next();
         }
       };
@@ -216,6 +222,9 @@ __global__ void __launch_bounds__(256, 1)
       };
       constexpr uint32_t idesc0 = idesc_bf16(256, C::kN0, 0, 1);
       constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
+      // A tile: two K-major [128 x 64] SW128 tiles; B tile: MN-major [128 k x 64] tiles 16 KB apart
+      auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
+      auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
       auto gemm0 = [&](int T, int kb0, int kb1) {
         if (kb0 == 0) {
           FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, (T & 1) ^ 1));
@@ -227,16 +236,13 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t sb = base + stage * C::kSTAGE;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
-            const uint64_t ad = desc_kmajor_sw128(sb + kk * 32);
+            const uint64_t ad = a_desc(sb, kk);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             if (kGated) {
-              const uint64_t b0 = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
-              const uint64_t b1 = desc_mnmajor_sw128(sb + C::kA_BYTES + C::BK * C::kBH * 2 + kk * 2048, 8192);
-              umma_bf16_pair(tmem_base, ad, b0, idesc0, acc);
-              umma_bf16_pair(tmem_base + C::kN0, ad, b1, idesc0, acc);
+              umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
+              umma_bf16_pair(tmem_base + C::kN0, ad, b_desc(sb + C::kSLOT + C::kSLOT / 2, kk), idesc0, acc);
             } else {
-              const uint64_t bd = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
-              umma_bf16_pair(tmem_base, ad, bd, idesc0, acc);
+              umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
             }
           }
           umma_commit_pair(empty_bar(stage), kPairMask);
@@ -261,12 +267,11 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t ab = (h == 0) ? own_slot + kb2 * (C::BM * C::BK * 2) : sb;
+          const uint32_t aslot = (h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
-            const uint64_t ad = desc_kmajor_sw128(ab + kk * 32);
-            const uint64_t bd = desc_mnmajor_sw128(sb + C::kA_BYTES + kk * 2048, 8192);
-            umma_bf16_pair(tmem_base + C::kTMEM_E, ad, bd, idesc1, e_started ? 1u : 0u);
+            umma_bf16_pair(tmem_base + C::kTMEM_E, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
+                           e_started ? 1u : 0u);
             e_started = true;
           }
           umma_commit_pair(empty_bar(stage), kPairMask);
@@ -297,8 +302,11 @@ __global__ void __launch_bounds__(256, 1)
     const int wq = warp & 3;
     const int row = wq * 32 + (int)lane_id();
     const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
+    const bool issuer = (warp == 4 && lane_id() == 0);
     unsigned long long w_cfull = 0, w_ofree = 0, t_drain = 0, t_store = 0, t_e = 0;
     const unsigned long long t_start = clock64();
+    // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
+    auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
     for (int T = 0; T < total_steps; ++T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
@@ -322,12 +330,11 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-        const int sub = c0 / 64;
+        const uint32_t tile = own_slot + (c0 / 64) * 16384;
         const int ch = (c0 % 64) / 8;
-        const uint32_t rowb = own_slot + sub * (C::BM * C::BK * 2) + row * 128;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          st_shared_v4(rowb + (((ch + j) ^ (row & 7)) << 4), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
         const int grow = u.m0 + (int)q * C::BM + row;
         if (args.c_debug != nullptr && grow < args.M) {
           const int ncol = u.n0 + (t * G + p) * C::kN0 + c0;
@@ -344,11 +351,11 @@ __global__ void __launch_bounds__(256, 1)
       const unsigned long long t_s0 = args.prof ? clock64() : 0ull;
       if (G > 1) {
         named_bar_sync(1, 128);
-        if (warp == 4 && lane_id() == 0) {
-          const int ncol = u.n0 + (t * G + p) * C::kN0;
+        if (issuer) {
+          const int nblk = (u.n0 + (t * G + p) * C::kN0) / 64;
 #pragma unroll
-          for (int sub = 0; sub < C::kCW / 64; ++sub)
-            tma_store_2d(&tmC, own_slot + sub * (C::BM * C::BK * 2), ncol + 64 * sub, u.m0 + (int)q * C::BM);
+          for (int j = 0; j < C::kCW / 128; ++j)
+            tma_store_3d(&maps.c, own_slot + j * 32768, 0, u.m0 + (int)q * C::BM, nblk + 2 * j);
           bulk_commit();
           bulk_wait0();
           fence_proxy_async_global();
@@ -358,35 +365,61 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (args.prof) t_store += clock64() - t_s0;
       if (t == steps - 1) {
+        // E slice: TMEM -> registers -> SW128 smem tiles in the own slot -> TMA
+        // store (bf16) or TMA reduce-add into the fp32 workspace (N splits).
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait_cluster(e_full, (T / steps) & 1);
         tc_fence_after();
-        const int grow = u.m0 + (int)q * C::BM + row;
+        mbar_wait_cluster(own_free, T & 1);  // own slot no longer read by hop 0 / the C store
+        const int erow = u.m0 + (int)q * C::BM;
+        constexpr int kTiles = C::kCHUNK_BYTES / 16384;  // 16 KB staging tiles in the own slot
+        const bool bf16_out = (args.S == 1);
+        const int cols_per_tile = bf16_out ? 64 : 32;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kLB; c0 += 32) {
-          float v[32];
-          tmem_ld32(lane_base + C::kTMEM_E + c0, v);
-          if (grow < args.M) {
-            if (args.S == 1) {
+        for (int g0 = 0; g0 < kLB; g0 += cols_per_tile * kTiles) {
+          const int g1 = (g0 + cols_per_tile * kTiles < kLB) ? g0 + cols_per_tile * kTiles : kLB;
+#pragma unroll 1
+          for (int c0 = g0; c0 < g1; c0 += 32) {
+            float v[32];
+            tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+            const uint32_t tile = own_slot + ((c0 - g0) / cols_per_tile) * 16384;
+            if (bf16_out) {
               uint32_t pk[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-              uint4* dst = reinterpret_cast<uint4*>(args.E + (size_t)grow * args.L + u.l0 + c0);
+              const int ch = (c0 % 64) / 8;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+              for (int j = 0; j < 4; ++j)
+                st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
             } else {
-              float* dst = args.ws + (size_t)grow * args.L + u.l0 + c0;
 #pragma unroll
-              for (int i = 0; i < 32; i += 4) red_add_v4_f32(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+              for (int j = 0; j < 8; ++j)
+                st_shared_v4(swz(tile, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
             }
           }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (issuer) {
+            for (int c0 = g0; c0 < g1; c0 += cols_per_tile) {
+              const uint32_t tile = own_slot + ((c0 - g0) / cols_per_tile) * 16384;
+              if (bf16_out)
+                tma_store_2d(&maps.e, tile, u.l0 + c0, erow);
+              else
+                tma_reduce_add_2d(&maps.w, tile, u.l0 + c0, erow);
+            }
+            bulk_commit();
+            bulk_wait_read0_group();
+          }
+          named_bar_sync(1, 128);
         }
         tc_fence_before();
         mbar_arrive_remote(L_e_empty);
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
-    if (args.prof && warp == 4 && lane_id() == 0) {
+    if (issuer) bulk_wait0();  // every E store / reduction performed before exit
+    if (args.prof && issuer) {
       unsigned long long* pr = args.prof + blockIdx.x * 16;
       pr[9] = clock64() - t_start;
       pr[10] = w_cfull;

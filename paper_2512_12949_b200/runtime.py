@@ -21,7 +21,7 @@ _workspaces: dict = {}
 
 def chain_desc(graph: ChainGraph) -> nat.ChainDesc:
     d = graph.dims
-    return nat.ChainDesc(nat.KIND[graph.kind], nat.ACT[graph.activation], d.m, d.n, d.k, d.l, 2)
+    return nat.ChainDesc(nat.KIND[graph.kind], nat.ACT[graph.activation], d.m, d.n, d.k, d.l, d.element_size)
 
 
 def plan_desc(plan: FusionPlan) -> nat.PlanDesc:
@@ -47,12 +47,25 @@ def _num_sms() -> int:
 EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2, "pair": nat.XCHG_L2_PAIR}
 
 
+def exchange_name(cfg: nat.KernelConfig) -> str:
+    return {v: k for k, v in EXCHANGES.items()}[int(cfg.exchange)]
+
+
 def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None,
-          exchange: str = "l2") -> nat.KernelConfig:
+          exchange: str = "auto") -> nat.KernelConfig:
     """Physical launch configuration for (graph, plan).  plan=None lets the
     runtime choose the hardware-shaped configuration; ``exchange`` picks the
-    shuffle transport: "dsm" (thread-block cluster, distributed shared memory)
-    or "l2" (TMA through an L2-resident scratch)."""
+    shuffle transport: "dsm" (thread-block cluster, distributed shared memory),
+    "l2" (TMA through an L2-resident scratch), "pair" (L2 transport, CTA-pair
+    cta_group::2 kernel) or "auto" (first of pair, l2, dsm that supports it)."""
+    if exchange == "auto":
+        last = None
+        for candidate in ("pair", "l2", "dsm"):
+            try:
+                return lower(graph, plan, num_sms, candidate)
+            except nat.UnsupportedPlan as exc:
+                last = exc
+        raise last
     lib = nat.load()
     cfg = nat.KernelConfig()
     ch = chain_desc(graph)
@@ -95,6 +108,8 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
         t = tensors[name]
         if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
+        if t.data_ptr() % 16:
+            raise ValueError(f"{name} must be 16-byte aligned")
     a = tensors["A"]
     if out is None:
         out = torch.empty((d.m, d.l), dtype=torch.bfloat16, device=a.device)
@@ -116,7 +131,7 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
 
 
 def run(graph: ChainGraph, plan: Optional[FusionPlan], tensors: dict, out=None, stream=None,
-        exchange: str = "l2"):
+        exchange: str = "auto"):
     """Execute the chain under ``plan`` on the current GPU; returns E (bf16)."""
     return launch(graph, lower(graph, plan, _num_sms(), exchange), tensors, out=out, stream=stream)
 

@@ -12,10 +12,14 @@ def ref(A,B,D,act,B1=None):
     elif act==3: c=torch.nn.functional.gelu(c, approximate='tanh')
     cb=c.bfloat16()
     return (cb.float()@D.float()), cb
+PACK=[True]
 def setup(m,n,k,l,act,gated,cfg,xchg):
     A=(torch.rand(m,k,device='cuda')*2-1).bfloat16()
-    B=(torch.rand(k,n,device='cuda')*2-1).bfloat16()
-    B1=(torch.rand(k,n,device='cuda')*2-1).bfloat16() if gated else B
+    if gated and PACK[0]:
+        B01=(torch.rand(2,k,n,device='cuda')*2-1).bfloat16(); B, B1 = B01[0], B01[1]
+    else:
+        B=(torch.rand(k,n,device='cuda')*2-1).bfloat16()
+        B1=(torch.rand(k,n,device='cuda')*2-1).bfloat16() if gated else B
     D=(torch.rand(n,l,device='cuda')*2-1).bfloat16()
     E=torch.zeros(m,l,device='cuda',dtype=torch.bfloat16)
     ch=nat.ChainDesc(1 if gated else 0, 2 if gated else act, m,n,k,l,2)
@@ -48,15 +52,18 @@ cases=[(128,128,64,64,0,False,(1,1,128,64)),(128,256,128,256,1,False,(1,1,128,25
        (3136,64,576,256,1,False,None),(512,3072,768,768,3,False,None),(512,8192,2048,2048,2,True,None),(512,16384,4096,4096,1,False,None),
        (1024,8192,2048,2048,1,False,None)]
 pair_cases=[(256,256,128,256,1,False,(1,1,256,256)),(256,512,128,512,1,False,(2,1,256,256)),(512,1024,256,1024,1,False,(4,1,256,256)),
-            (512,1024,256,1024,1,False,(4,2,256,256)),(256,512,256,256,2,True,(1,1,128,256)),(256,1024,256,512,2,True,(2,2,128,256)),
-            (200,1536,256,768,3,False,(3,2,256,256)),(512,1024,256,512,1,False,(4,1,256,128)),
-            (3136,512,576,256,1,False,None),(512,3072,768,768,3,False,None),(512,8192,2048,2048,2,True,None),(512,16384,4096,4096,1,False,None),
-            (1024,8192,2048,2048,1,False,None)]
-for c in pair_cases:
-    try:
-        run(*c, xchg=2)
-    except Exception as e:
-        print("FAIL", 2, c, repr(e), flush=True)
+            (512,2048,256,1024,1,False,(4,2,256,256)),(256,512,256,256,2,True,(1,1,128,256)),(256,1024,256,512,2,True,(2,2,128,256)),
+            (200,1536,256,768,3,False,(3,2,256,256)),(3136,512,640,256,1,False,None),(512,3072,768,768,3,False,None),
+            (512,8192,2048,2048,2,True,None),(512,16384,4096,4096,1,False,None),(1024,8192,2048,2048,1,False,None)]
+for pack in (True, False):
+    PACK[0]=pack
+    for c in pair_cases:
+        if not pack and not c[5]: continue
+        try:
+            run(*c, xchg=2)
+        except Exception as e:
+            print("FAIL", 2, c, repr(e), flush=True)
+PACK[0]=True
 for xchg in ([] if len(sys.argv) > 1 else (1,0)):
     for c in cases:
         try:

@@ -1,0 +1,201 @@
+"""GPU parity: the sm_100a fused chain (through the C ABI / public API) against
+the CPU oracle on the same seeded inputs.
+
+Tolerance (north star): max-abs relative error <= 1e-2 against the fp32 chain
+computed from the bf16-rounded inputs (simulator.py:143-147 metric).  The
+oracle also rounds the intermediate C to bf16 (the GPU's dataflow); the
+unrounded fp32 oracle is checked too at the same bound."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-2
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _graph(kind, act, m, n, k, l):
+    from paper_2512_12949_b200 import workload as W
+
+    d = W.DimensionSpec(m, n, k, l, 2)
+    return W.build_gated_ffn(d) if kind == "gated_ffn" else W.build_standard_ffn(d, act)
+
+
+def _inputs(kind, m, n, k, l, seed, packed=True):
+    torch = _torch()
+    host = {name: oracle.round_bf16(v) for name, v in oracle.make_inputs(kind, m, n, k, l, seed=seed).items()}
+    dev = {name: torch.from_numpy(v).cuda().to(torch.bfloat16) for name, v in host.items()}
+    if kind == "gated_ffn" and packed:  # gate|up packed [2][K][N]
+        w = torch.stack([dev["B0"], dev["B1"]])
+        dev["B0"], dev["B1"] = w[0], w[1]
+    return host, dev
+
+
+def _check(kind, act, host, out):
+    got = out.float().cpu().numpy()
+    ref_b = oracle.dense_chain(kind, act, host, bf16_intermediate=True)
+    ref = oracle.dense_chain(kind, act, host)
+    err_b = oracle.max_relative_error(got, ref_b)
+    err = oracle.max_relative_error(got, ref)
+    assert np.isfinite(got).all()
+    assert err_b <= TOL and err <= TOL, (err_b, err)
+    return err_b
+
+
+CASES = [
+    ("standard_ffn", "relu", 256, 1024, 256, 1024),
+    ("standard_ffn", "identity", 128, 512, 128, 256),
+    ("standard_ffn", "silu", 256, 2048, 512, 512),
+    ("standard_ffn", "gelu", 512, 3072, 768, 768),          # GPT-2 small FFN, full size
+    ("gated_ffn", "silu", 256, 1024, 512, 512),
+    ("gated_ffn", "silu", 512, 8192, 2048, 2048),           # LLaMA-1B SwiGLU, full size
+    ("standard_ffn", "relu", 200, 768, 256, 768),           # ragged M (not a tile multiple)
+    ("standard_ffn", "relu", 3136, 64, 576, 256),           # conv C5 implicit GEMM (im2col view)
+    ("standard_ffn", "relu", 40, 256, 128, 256),            # M smaller than one tile
+]
+
+
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
+def test_fused_chain_matches_oracle(case, exchange):
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    try:
+        cfg = runtime.lower(graph, None, 148, exchange)
+    except nat.UnsupportedPlan:
+        pytest.skip(f"{exchange} has no lowering for {case}")
+    host, dev = _inputs(kind, m, n, k, l, seed=17)
+    out = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    _check(kind, act, host, out)
+    # relaunch with the same workspace (epoch-stamped flags, reused scratch)
+    out2 = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    assert _torch().equal(out, out2) or _check(kind, act, host, out2) <= TOL
+
+
+@pytest.mark.parametrize("ring,splits,nb,lb,exchange", [(1, 1, 128, 256, "l2"), (2, 1, 128, 256, "dsm"),
+                                                        (4, 2, 128, 256, "l2"), (8, 1, 128, 128, "dsm"),
+                                                        (4, 1, 64, 256, "l2"), (3, 2, 256, 256, "pair"),
+                                                        (4, 2, 256, 256, "pair")])
+def test_explicit_configs(ring, splits, nb, lb, exchange):
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    m, k = 256, 256
+    l = ring * lb
+    n = splits * ring * nb * 3
+    graph = _graph("standard_ffn", "relu", m, n, k, l)
+    cfg = nat.KernelConfig()
+    cfg.ring, cfg.n_splits, cfg.nb, cfg.lb, cfg.exchange = ring, splits, nb, lb, runtime.EXCHANGES[exchange]
+    host, dev = _inputs("standard_ffn", m, n, k, l, seed=ring * 10 + splits)
+    out = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    _check("standard_ffn", "relu", host, out)
+
+
+def test_intermediate_c_matches_oracle():
+    """The bf16 intermediate the kernel materialises on chip equals act(A@B)."""
+    torch = _torch()
+    from paper_2512_12949_b200 import runtime
+
+    graph = _graph("standard_ffn", "gelu", 256, 1024, 256, 512)
+    host, dev = _inputs("standard_ffn", 256, 1024, 256, 512, seed=4)
+    for exchange in ("dsm", "l2", "pair"):
+        cfg = runtime.lower(graph, None, 148, exchange)
+        c_dbg = torch.zeros((256, 1024), dtype=torch.bfloat16, device="cuda")
+        runtime.launch(graph, cfg, dev, c_debug=c_dbg)
+        torch.cuda.synchronize()
+        c_ref = oracle.gelu_tanh(host["A"].astype(np.float64) @ host["B"])
+        assert oracle.max_relative_error(c_dbg.float().cpu().numpy(), c_ref) <= TOL
+
+
+def test_reference_plans_execute_through_public_api():
+    """Top plans of the reference search (golden, B200 profile) run through
+    execute_plan -- the drop-in for simulator.execute_plan -- with the traffic
+    trace equal to the analyzer's prediction."""
+    import paper_2512_12949_b200 as ff
+    from paper_2512_12949_b200 import workload as W
+    from paper_2512_12949_b200.hardware import b200_profile
+    from paper_2512_12949_b200.plan import plan_from_dict
+
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "search_results.json")))
+    dev = b200_profile()
+    ran = 0
+    for name in ("b200_gpt2s", "b200_llama1b", "b200_conv_c5"):
+        g = gold[name]["graph"]
+        dims = W.DimensionSpec(g["m"], g["n"], g["k"], g["l"], 2)
+        graph = W.build_gated_ffn(dims) if g["kind"] == "gated_ffn" else W.build_standard_ffn(
+            dims, g["activation"], logical_m=g.get("logical_m"))
+        plan = plan_from_dict(gold[name]["result"]["top"][0]["plan"])
+        inputs = ff.make_inputs(graph, ff.SimConfig(seed=2))
+        rounded = {k: oracle.round_bf16(v) for k, v in inputs.items()}
+        out, trace = ff.execute_plan(plan, graph, rounded, ff.SimConfig(), dev)
+        ref = oracle.dense_chain(graph.kind, graph.activation, rounded)
+        assert oracle.max_relative_error(out, ref) <= TOL, name
+        assert trace.tier_bytes == ff.analyze(graph, dev, plan).volume
+        ran += 1
+    assert ran == 3
+
+
+def test_verify_report():
+    import paper_2512_12949_b200 as ff
+    from paper_2512_12949_b200.hardware import b200_profile
+    from paper_2512_12949_b200.plan import make_plan
+
+    graph = ff.build_gated_ffn(ff.DimensionSpec(256, 1024, 512, 512))
+    plan = make_plan("n", "klm", (64, 128, 1024, 256), (1, 2, 1, 2), "doubled_k")
+    rep = ff.verify(plan, graph, ff.SimConfig(seed=9), device=b200_profile())
+    assert rep.passed, rep.to_dict()
+
+
+@pytest.mark.parametrize("name", ["gpt67b", "opt13b_m4096"])
+def test_large_baseline_configs(name):
+    """Full BASELINE sizes against the CPU oracle (f32 numpy)."""
+    import bench
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
+    graph = _graph(kind, act, m, n, k, l)
+    host, dev = _inputs(kind, m, n, k, l, seed=23)
+    out = runtime.run(graph, None, dev)
+    _torch().cuda.synchronize()
+    _check(kind, act, host, out)
+
+
+def test_two_streams_and_rejections():
+    torch = _torch()
+    from paper_2512_12949_b200 import runtime
+
+    graph = _graph("standard_ffn", "relu", 256, 1024, 256, 1024)
+    host, dev = _inputs("standard_ffn", 256, 1024, 256, 1024, seed=5)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        o1 = runtime.run(graph, None, dev, stream=s1, exchange="dsm")
+    with torch.cuda.stream(s2):
+        o2 = runtime.run(graph, None, dev, stream=s2, exchange="dsm")
+    torch.cuda.synchronize()
+    _check("standard_ffn", "relu", host, o1)
+    _check("standard_ffn", "relu", host, o2)
+    with pytest.raises(ValueError):
+        bad = dict(dev)
+        bad["A"] = dev["A"].float()
+        runtime.run(graph, None, bad)
+    with pytest.raises(ValueError):
+        bad = dict(dev)
+        bad["D"] = dev["D"].t()
+        runtime.run(graph, None, bad)

@@ -1,0 +1,137 @@
+"""The C-ABI library loads, exports exactly what include/*.h declares, its
+struct layouts match the ctypes mirror, and the (host-only) lowering entry
+points behave -- no GPU needed."""
+
+import ctypes
+import json
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2512_12949_b200 import _native as nat
+from paper_2512_12949_b200 import runtime
+from paper_2512_12949_b200 import workload as W
+from paper_2512_12949_b200.errors import PlanError
+from paper_2512_12949_b200.plan import make_plan, plan_from_dict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INC = os.path.join(ROOT, "include")
+
+
+def declared_symbols():
+    names = set()
+    for fname in os.listdir(INC):
+        text = open(os.path.join(INC, fname)).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(ff_\w+)\s*\(", text))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_12949_b200 import build
+
+    build.build()
+    return nat.load()
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", nat.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ff_\w+)", out))
+    declared = declared_symbols()
+    assert declared, "no declarations parsed"
+    assert declared <= exported, f"missing: {declared - exported}"
+    assert set(nat.EXPORTS) <= exported
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "ff_chain.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(ffChainDesc), sizeof(ffPlanDesc),'
+                   ' sizeof(ffKernelConfig), sizeof(ffTensors));return 0;}\n')
+    exe = tmp_path / "sz"
+    subprocess.run(["gcc", "-I", INC, str(src), "-o", str(exe)], check=True)
+    sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    assert sizes == [ctypes.sizeof(nat.ChainDesc), ctypes.sizeof(nat.PlanDesc), ctypes.sizeof(nat.KernelConfig),
+                     ctypes.sizeof(nat.Tensors)]
+
+
+def _check_cfg(graph, cfg):
+    d = graph.dims
+    width = 2 if cfg.exchange == nat.XCHG_L2_PAIR else 1
+    assert d.l % (cfg.ring * cfg.lb) == 0
+    assert d.n % (cfg.n_splits * cfg.ring * cfg.nb) == 0
+    assert cfg.m_tiles == -(-d.m // (128 * width))
+    assert cfg.units == cfg.m_tiles * cfg.l_clusters * cfg.n_splits
+    assert 1 <= cfg.rings <= cfg.units
+    assert cfg.grid_ctas == cfg.rings * cfg.ring * width <= 148
+    if cfg.exchange == nat.XCHG_DSM:
+        assert cfg.ring <= 16
+
+
+def test_lowering_of_reference_top_plans(lib):
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "search_results.json")))
+    lowered = 0
+    for name, case in gold.items():
+        if not name.startswith("b200_"):
+            continue
+        g = case["graph"]
+        dims = W.DimensionSpec(g["m"], g["n"], g["k"], g["l"], 2)
+        graph = W.build_gated_ffn(dims) if g["kind"] == "gated_ffn" else W.build_standard_ffn(dims, "relu")
+        for entry in case["result"]["top"][:3]:
+            plan = plan_from_dict(entry["plan"])
+            for exchange in ("dsm", "l2", "pair"):
+                try:
+                    cfg = runtime.lower(graph, plan, 148, exchange)
+                except nat.UnsupportedPlan:
+                    continue
+                _check_cfg(graph, cfg)
+                lowered += 1
+    assert lowered >= 10
+
+
+@pytest.mark.parametrize("dims,kind", [((512, 8192, 2048, 2048), "gated_ffn"), ((512, 16384, 4096, 4096), "standard_ffn"),
+                                       ((512, 3072, 768, 768), "standard_ffn"), ((3136, 64, 576, 256), "standard_ffn"),
+                                       ((4096, 8192, 2048, 2048), "standard_ffn"), ((200, 768, 256, 768), "standard_ffn")])
+def test_auto_config_invariants(lib, dims, kind):
+    d = W.DimensionSpec(*dims, 2)
+    graph = W.build_gated_ffn(d) if kind == "gated_ffn" else W.build_standard_ffn(d, "relu")
+    ok = 0
+    for exchange in ("dsm", "l2", "pair"):
+        try:
+            cfg = runtime.lower(graph, None, 148, exchange)
+        except nat.UnsupportedPlan:
+            continue
+        _check_cfg(graph, cfg)
+        ok += 1
+    assert ok >= 1
+
+
+def test_status_codes_map_to_reference_exceptions(lib):
+    graph = W.build_standard_ffn(W.DimensionSpec(256, 1024, 256, 1024, 2), "relu")
+    bad = make_plan("ml", "nk", (64, 256, 256, 256), (1, 4, 1, 4))  # l grid-spatial (Rule 4)
+    with pytest.raises(PlanError):
+        runtime.lower(graph, bad, 148, "dsm")
+    gated_plan_on_standard = make_plan("n", "klm", (64, 256, 256, 256), (1, 4, 1, 4), "doubled_k")
+    with pytest.raises(PlanError):
+        runtime.lower(graph, gated_plan_on_standard, 148, "l2")
+    odd = W.build_standard_ffn(W.DimensionSpec(256, 1000, 256, 1024, 2), "relu")  # n not a multiple of 64
+    with pytest.raises(nat.UnsupportedPlan):
+        runtime.lower(odd, None, 148, "l2")
+    f32 = W.build_standard_ffn(W.DimensionSpec(256, 1024, 256, 1024, 4), "relu")
+    with pytest.raises(nat.UnsupportedPlan):
+        runtime.lower(f32, None, 148, "l2")
+
+
+def test_workspace_sizes(lib):
+    graph = W.build_standard_ffn(W.DimensionSpec(512, 16384, 4096, 4096, 2), "relu")
+    for exchange in ("dsm", "l2", "pair"):
+        cfg = runtime.lower(graph, None, 148, exchange)
+        ch = runtime.chain_desc(graph)
+        need = lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(cfg))
+        if cfg.n_splits > 1:
+            assert need >= 512 * 4096 * 4
+        if exchange != "dsm" and cfg.ring > 1:
+            assert need >= 512 * 16384 * 2

@@ -1,0 +1,80 @@
+"""Token (M) sharding across ranks: host logic and a world-size-2 gloo run
+(CPU).  Each rank computes its rows with the CPU oracle standing in for the
+GPU chain; the all-gathered result equals the unsharded chain."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2512_12949_b200 import sharding
+from paper_2512_12949_b200 import workload as W
+
+
+@pytest.mark.parametrize("m,world", [(512, 2), (32768, 8), (3136, 4), (200, 3), (16, 2), (100, 8)])
+def test_shard_bounds_partition_rows(m, world):
+    spans = [sharding.shard_bounds(m, world, r) for r in range(world)]
+    assert spans[0][0] == 0 and spans[-1][1] == m
+    for (a, b), (c, d) in zip(spans, spans[1:]):
+        assert b == c and a <= b
+    sizes = [b - a for a, b in spans]
+    assert max(sizes) - min(sizes) <= sharding.ROW_GRANULE
+    assert all(a % sharding.ROW_GRANULE == 0 for a, _ in spans)
+
+
+def test_shard_graph_dims():
+    g = W.build_gated_ffn(W.DimensionSpec(32768, 8192, 2048, 2048))
+    for r in range(8):
+        sub = sharding.shard_graph(g, 8, r)
+        assert sub.dims.m == 4096 and sub.kind == g.kind and sub.dims.n == 8192
+    tiny = W.build_standard_ffn(W.DimensionSpec(48, 64, 64, 64), "relu")
+    parts = [sharding.shard_graph(tiny, 4, r) for r in range(4)]
+    assert sum(p is not None for p in parts) == 3
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, n, k, l = 96, 64, 32, 48
+    inputs = oracle.make_inputs("standard_ffn", m, n, k, l, seed=3, dtype=np.float32)
+    lo, hi = sharding.shard_bounds(m, world, rank)
+    local = dict(inputs)
+    local["A"] = inputs["A"][lo:hi]
+    part = torch.from_numpy(oracle.dense_chain("standard_ffn", "relu", local))
+    sizes = [sharding.shard_bounds(m, world, r) for r in range(world)]
+    parts = [torch.empty((b - a, l)) for a, b in sizes]
+    dist.all_gather(parts, part)
+    full = torch.cat(parts).numpy()
+    ref = oracle.dense_chain("standard_ffn", "relu", inputs)
+    # max over ranks of a per-rank "time", the way bench.py reduces device timings
+    t = torch.tensor([float(rank + 1)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    q.put((rank, float(np.max(np.abs(full - ref))), float(t.item())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_sharded_chain_equals_unsharded():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, err, tmax in results:
+        assert err <= 1e-4
+        assert tmax == 2.0
