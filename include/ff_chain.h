@@ -115,9 +115,11 @@ int ff_auto_config(const ffChainDesc* chain, int32_t num_sms, ffKernelConfig* ou
 /* Same, with an explicit shuffle transport. */
 int ff_auto_config_ex(const ffChainDesc* chain, int32_t num_sms, int32_t exchange, ffKernelConfig* out);
 
-/* Workspace (device bytes) the launch needs; 0 when none.  The workspace must be
- * zero-filled once when first allocated; it never needs clearing again (the L2
- * transport's ready flags are epoch-stamped). */
+/* Workspace (device bytes) the launch needs.  The workspace must be zero-filled
+ * once when first allocated; it never needs clearing again (the L2 transport's
+ * ready flags are epoch-stamped; split-N counters and the fp32 E region are
+ * re-zeroed by the last contributor of each tile).  Launches that may run
+ * concurrently (different streams) need separate workspaces. */
 size_t ff_chain_workspace_bytes(const ffChainDesc* chain, const ffKernelConfig* cfg);
 
 /* Execute the fused chain with an explicit physical configuration.
@@ -136,8 +138,9 @@ int ff_chain_launch_debug(const ffChainDesc* chain, const ffKernelConfig* cfg, c
 /* Number of CUDA kernels one ff_chain_launch issues (for launch accounting). */
 int ff_chain_kernel_count(const ffChainDesc* chain, const ffKernelConfig* cfg);
 
-/* Diagnostics: device buffer of unsigned long long[grid_ctas][16] that receives
- * per-CTA wait-cycle counters on every launch (NULL disables; default). */
+/* Diagnostics: device buffer of unsigned long long[grid_ctas][32] that receives
+ * per-CTA wait-cycle counters (slots 0-15) and globaltimer stamps (16-31) on
+ * every launch (NULL disables; default). */
 void ff_set_profile_buffer(void* dev_ptr);
 
 /* Thread-local message for the last non-OK status. */

@@ -17,6 +17,20 @@ int ff_dsm_push_bench(int cluster, int chunk_bytes, int depth, int iters, int nu
 /* cudaOccupancyMaxActiveClusters for a `cluster`-CTA launch using `smem_bytes`. */
 int ff_max_active_clusters(int cluster, int smem_bytes, int* out);
 
+/* TMA streaming benchmark (per-SM operand feed vs box shape): `ctas` CTAs each
+ * stream `iters` stages of `stage_bytes` from a bf16 [rows][cols] matrix in 3D
+ * boxes {64, box_rows & 0xffff, box_rows >> 16} (2D {64, box_rows} when the high
+ * half is 0) with `stages` in flight and `producers` issuing threads. */
+int ff_tma_stream_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows, int ctas,
+                        int producers, int stage_bytes, float* ms_out);
+
+/* Same with TMA multicast: clusters of `csize` CTAs; each CTA fetches 1/csize of
+ * every {64, box_rows, box_blocks} box and multicasts it to the whole cluster.
+ * flags (csize == 1): bit0 plain non-cluster launch, bit1 producer waits with CTA
+ * scope, bit2 consumer arrives locally (else acquire/release.cluster forms). */
+int ff_tma_mcast_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows, int box_blocks,
+                       int csize, int ctas, int stage_bytes, int flags, float* ms_out);
+
 const char* ff_dsm_last_error(void);
 
 #ifdef __cplusplus

@@ -197,6 +197,69 @@ __global__ void __launch_bounds__(256, 1) tma_stream_kernel(const __grid_constan
   }
   __syncthreads();
 }
+// Multicast variant: clusters of `csize` CTAs stream the same 3D tiles; CTA r
+// of a cluster fetches slice r (box rows / csize) of every stage-sized tile
+// and multicasts it to all CTAs, so each CTA receives `stage_bytes` per stage
+// while issuing 1/csize of them.  Measures whether multicast lifts the per-SM
+// operand feed above the single-CTA TMA ceiling.
+__global__ void __launch_bounds__(256, 1) tma_mcast_kernel(const __grid_constant__ CUtensorMap map, int rows,
+                                                           int cols, int stages, int iters, int box_rows,
+                                                           int box_blocks, int stage_bytes, int flags) {
+  using namespace ff;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t base = (smem_u32(smem) + 1023u) & ~1023u;
+  const uint32_t full0 = base + stages * stage_bytes, empty0 = full0 + 8 * stages;
+  const int csize = (int)cluster_size(), me = (int)cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, csize);  // every CTA's consumer frees the stage cluster-wide
+    }
+    fence_mbar_init();
+  }
+  cluster_sync();
+  const int slice_rows = box_rows / csize;
+  const int slice_bytes = 64 * slice_rows * 2 * box_blocks;
+  const int per_box = 64 * box_rows * 2 * box_blocks;
+  const int boxes = stage_bytes / per_box;
+  const int col_tiles = cols / (64 * box_blocks), row_tiles = rows / box_rows;
+  const int cl = blockIdx.x / csize;
+  const uint16_t mask = (uint16_t)((1u << csize) - 1u);
+  const bool cta_wait = (flags & 2) != 0;    // csize == 1 only: producer waits with CTA scope
+  const bool cta_arrive = (flags & 4) != 0;  // csize == 1 only: consumer arrives locally (no release.cluster)
+  if (threadIdx.x == 0) {
+    int stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      if (cta_wait)
+        mbar_wait(empty0 + 8 * stage, phase ^ 1);
+      else
+        mbar_wait_cluster(empty0 + 8 * stage, phase ^ 1);
+      mbar_expect_tx(full0 + 8 * stage, stage_bytes);
+      for (int b = 0; b < boxes; ++b) {
+        const long long lin = (long long)cl * 7919 + (long long)i * boxes + b;
+        const int ct = (int)(lin % col_tiles), rt = (int)((lin / col_tiles) % row_tiles);
+        const uint32_t dst = base + stage * stage_bytes + b * per_box + me * slice_bytes;
+        if (csize > 1)
+          tma_load_3d_mcast(dst, &map, full0 + 8 * stage, 0, rt * box_rows + me * slice_rows, ct * box_blocks, mask);
+        else
+          tma_load_3d(dst, &map, full0 + 8 * stage, 0, rt * box_rows, ct * box_blocks);
+      }
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    }
+  } else if (threadIdx.x == 128) {
+    int stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(full0 + 8 * stage, phase);
+      if (cta_arrive)
+        mbar_arrive(empty0 + 8 * stage);
+      else
+        for (int r = 0; r < csize; ++r) mbar_arrive_remote(mapa(empty0 + 8 * stage, r));
+      if (++stage == stages) { stage = 0; phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+}
 }  // namespace
 
 extern "C" int ff_tma_stream_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows,
@@ -244,6 +307,60 @@ extern "C" int ff_tma_stream_bench(const void* mat, int rows, int cols, int stag
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   if (e != cudaSuccess) return 4;
+  *ms_out = ms;
+  return 0;
+}
+
+extern "C" int ff_tma_mcast_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows,
+                                  int box_blocks, int csize, int ctas, int stage_bytes, int flags, float* ms_out) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess) return 4;
+  if (csize < 1 || box_rows % csize || ctas % csize) return 5;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)cols / 64};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)(box_rows / csize), (cuuint32_t)box_blocks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult cr = reinterpret_cast<EncodeFn>(p)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(mat), dims,
+                                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return 6;
+  const int smem = stages * stage_bytes + 16 * stages + 2048;
+  if (smem > 232448) return 5;
+  cudaFuncSetAttribute(tma_mcast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(ctas, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = (flags & 1) && csize == 1 ? 0 : 1;  // bit0: plain (non-cluster) launch
+  if (csize > 1) flags &= ~6;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaLaunchKernelEx(&lc, tma_mcast_kernel, map, rows, cols, stages, 8, box_rows, box_blocks, stage_bytes, flags);
+  cudaEventRecord(a);
+  cudaLaunchKernelEx(&lc, tma_mcast_kernel, map, rows, cols, stages, iters, box_rows, box_blocks, stage_bytes, flags);
+  cudaEventRecord(b);
+  cudaError_t e = cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return 4;
+  }
   *ms_out = ms;
   return 0;
 }

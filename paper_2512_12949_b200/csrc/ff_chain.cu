@@ -115,29 +115,41 @@ int table_active_clusters(int cluster, int num_sms) {
 }
 
 struct WsLayout {
-  size_t e_off, c_off, f_off, total;
+  size_t e_off, c_off, f_off, n_off, total;
+  bool e_memset;  // fp32 E larger than the zero zone: clear it before the launch
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-// Workspace: [flags, fixed 1 MiB at offset 0 in EVERY layout][fp32 E][C scratch].
-// The flags region never holds anything but epoch stamps, whatever config
-// used the workspace before, so a stale stamp is always older than the
-// current launch's epoch.
+// Workspace: [flags: fixed 1 MiB at offset 0][split arrival counters: fixed
+// 256 KiB][fp32 E: fixed 32 MiB zone][C scratch].  The flags region only ever
+// holds epoch stamps, so a stale stamp is always older than the current
+// launch's epoch.  The counters and the fp32 E zone are zero between launches:
+// the last contributor of every E tile re-zeroes its tile and counter
+// (split_finish), and no config puts C scratch inside them, so a workspace
+// zero-filled once stays valid whatever configs share it.  A split chain whose
+// fp32 E exceeds the zone spills past it and clears it with a memset first.
 constexpr size_t kFlagBytes = 1u << 20;
+constexpr size_t kCntBytes = 256u << 10;
+constexpr size_t kEZoneBytes = 32u << 20;
 WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   WsLayout w{};
   const bool pair = c->exchange == FF_XCHG_L2_PAIR;
+  const size_t e_bytes = c->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
+  const bool c_scratch = c->exchange != FF_XCHG_DSM && c->ring > 1;
   w.f_off = 0;
-  size_t off = kFlagBytes;
-  w.e_off = off;
-  if (c->n_splits > 1) off = align256(off + (size_t)ch->m * ch->l * sizeof(float));
+  w.n_off = kFlagBytes;
+  w.e_off = kFlagBytes + kCntBytes;
+  w.e_memset = e_bytes > kEZoneBytes;
+  size_t off = w.e_off + e_bytes;
+  if (c_scratch) off = w.e_off + std::max(e_bytes, kEZoneBytes);
   w.c_off = off;
-  if (c->exchange != FF_XCHG_DSM && c->ring > 1) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
+  if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   w.total = off;
   return w;
 }
 
 std::atomic<uint32_t> g_epoch{0};
-unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA wait-cycle counters (ff_set_profile_buffer)
+unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
+uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
 
 template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
@@ -215,22 +227,18 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
+  a.tile_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
+  a.dbg = g_dbg;
 
-  if (cfg->n_splits > 1) {
-    cudaError_t e = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
-    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  if (wl.e_memset) {
+    cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
+    if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
-  if (cfg->n_splits > 1) {
-    const size_t n = (size_t)M * L;
-    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(a.ws, a.E, n);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
-  }
   return FF_OK;
 }
 
@@ -302,6 +310,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
+  if (cfg->ring > 64) return fail(FF_ERR_UNSUPPORTED, "ring of more than 64 pairs");
   const int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
   if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring of pairs larger than the GPU");
   ff::ChainArgs a{};
@@ -321,11 +330,13 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
+  a.tile_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
-  if (cfg->n_splits > 1) {
-    cudaError_t e = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
-    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  a.dbg = g_dbg;
+  if (wl.e_memset) {
+    cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
+    if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(rings * cfg->ring * 2, 1, 1);
@@ -349,11 +360,6 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     e = cudaLaunchKernelEx(&lc, kern, maps, a);
   }
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx(pair): ") + cudaGetErrorString(e));
-  if (cfg->n_splits > 1) {
-    ff::ff_finalize_kernel<<<num_sms_cached() * 4, 256, 0, stream>>>(a.ws, a.E, (size_t)M * L);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("finalize: ") + cudaGetErrorString(e));
-  }
   return FF_OK;
 }
 
@@ -464,6 +470,9 @@ const char* ff_last_error(void) { return g_last_error.c_str(); }
 // Diagnostics: when non-NULL, kernels write per-CTA wait-cycle counters
 // (unsigned long long[grid_ctas][16]) into this device buffer.
 void ff_set_profile_buffer(void* dev_ptr) { g_prof = reinterpret_cast<unsigned long long*>(dev_ptr); }
+// Diagnostics (not in the header's stable API): bit0 skip MMAs, bit1 skip ready-flag waits.
+// Results are wrong while set; used only by the feed-limit probes.
+void ff_set_debug_mode(int mode) { g_dbg = (uint32_t)mode; }
 const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
 
 int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {
@@ -563,7 +572,9 @@ size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg
 
 int ff_chain_kernel_count(const ffChainDesc* ch, const ffKernelConfig* cfg) {
   if (!ch || !cfg) return 0;
-  return cfg->n_splits > 1 ? 2 : 1;
+  // split-N reduction and the bf16 cast finish inside the chain kernel; only
+  // an fp32 E beyond the workspace's zero zone adds a memset
+  return ws_layout(ch, cfg).e_memset ? 2 : 1;
 }
 
 static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, const ffTensors* t, void* ws,
@@ -583,6 +594,8 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   if (cfg.exchange != FF_XCHG_DSM &&
       (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes)
     return fail(FF_ERR_UNSUPPORTED, "too many (unit, step, member) chunks for the flag region");
+  if (cfg.n_splits > 1 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / cfg.lb) * sizeof(uint32_t) > kCntBytes)
+    return fail(FF_ERR_UNSUPPORTED, "too many E tiles for the split arrival counters");
   if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(FF_ERR_ARG, "workspace must be 256-byte aligned");
   LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb, cfg.exchange);
   return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream));

@@ -27,8 +27,9 @@
 //         Requires a fully co-resident (cooperative) launch.
 //     GEMM1 hops of n-step t are interleaved with GEMM0 k-blocks of n-step t+1;
 //   * inter-cluster reduce: with S > 1 N splits the E tiles are combined with
-//     red.global.add.v4.f32 into an fp32 workspace, then cast to bf16
-//     (simulator.py:371 "+=" into E); with S == 1 E is stored in bf16;
+//     red.global.add.v4.f32 into an fp32 workspace; the last of the S
+//     contributors of a tile casts it to bf16 and re-zeroes it (split_finish;
+//     simulator.py:371 "+=" into E); with S == 1 E is stored in bf16;
 //   * persistent: each ring processes work units (m tile, l cluster, split)
 //     unit = ring_id, ring_id + n_rings, ...; every counter is global across
 //     units so the pipelines never drain between units.
@@ -60,10 +61,18 @@ struct ChainArgs {
   __nv_bfloat16* E;    // output (S == 1)
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
+  uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
-  unsigned long long* prof;  // optional: per-CTA wait-cycle counters [grid][16] (diagnostics)
+  uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits
+  unsigned long long* prof;  // optional diagnostics: per CTA [FF_PROF_STRIDE] = 16 wait-cycle counters + 16 globaltimer stamps
 };
 
+#define FF_PROF_STRIDE 32
+// Stamp timeline slot `i` (16..31) of this CTA with the global nanosecond timer.
+#define FF_STAMP(i)                                                        \
+  do {                                                                     \
+    if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + (i)] = globaltimer_ns(); \
+  } while (0)
 // Accumulate the cycles spent in `stmt` into `acc` when profiling is on.
 #define FF_TIMED(acc, stmt)                                           \
   do {                                                                \
@@ -72,19 +81,115 @@ struct ChainArgs {
     if (args.prof) acc += clock64() - _t0;                            \
   } while (0)
 
+// Activations on the MUFU tanh unit (tanh.approx.f32, rel. err ~2^-11, far
+// below the bf16 rounding of C that follows): silu(x) = x*sigmoid(x) with
+// sigmoid(x) = (1 + tanh(x/2)) / 2, gelu_tanh per its definition.  No IEEE
+// division (whose FCHK slow path serialised the C drain, profiles/r01).
+__device__ __forceinline__ float silu_fast(float x) {
+  const float h = 0.5f * x;
+  return fmaf(h, tanh_approx(h), h);
+}
 __device__ __forceinline__ float apply_act(int act, float x) {
   switch (act) {
     case ACT_RELU:
       return fmaxf(x, 0.0f);
     case ACT_SILU:
-      return x / (1.0f + __expf(-x));
+      return silu_fast(x);
     case ACT_GELU_TANH: {
       const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-      float u = k0 * (x + k1 * x * x * x);
-      return 0.5f * x * (1.0f + tanhf(u));
+      const float u = k0 * fmaf(k1 * x, x * x, x);
+      const float h = 0.5f * x;
+      return fmaf(h, tanh_approx(u), h);
     }
     default:
       return x;
+  }
+}
+
+// Activation over a register fragment, the switch hoisted out of the loop.
+template <int N>
+__device__ __forceinline__ void apply_act_frag(int act, float (&v)[N]) {
+  if (act == ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = fmaxf(v[i], 0.0f);
+  } else if (act == ACT_SILU) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = silu_fast(v[i]);
+  } else if (act == ACT_GELU_TANH) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = apply_act(ACT_GELU_TANH, v[i]);
+  }
+}
+
+// Split-N finish (the reference's inter_cluster_reduce "+=", simulator.py:
+// 380-404, plus the final cast): called by the 128 epilogue threads of a CTA
+// after its fp32 partial of E tile rows [row0, row0+128) x cols [col0, col0+kCols)
+// has been issued into the workspace (TMA reduce-add by `issuer`, or red.add by
+// every thread).  Each contributor bumps the tile's arrival counter.
+//   shared == false: the S-th (last) arrival reads the finished sum, writes bf16
+//     E and re-zeroes the tile and the counter.
+//   shared == true (every contributor is in its ring's final unit, so spinning
+//     cannot block another unit): each contributor waits for all S arrivals and
+//     finishes the row slice [ticket*128/S, (ticket+1)*128/S); the last to
+//     finish resets the counter.
+// Either way the workspace is zero again when the kernel exits (no memset or
+// cast kernel around the launch).  `row` = this thread's index 0..127.
+template <int kCols>
+__device__ __forceinline__ void split_finish(const ChainArgs& args, uint32_t* counter, uint32_t bcast, bool issuer,
+                                             bool tma_reduce, int row0, int row, int col0, uint32_t bar_id,
+                                             bool shared) {
+  const uint32_t S = (uint32_t)args.S;
+  if (!tma_reduce) __threadfence();  // this thread's red.add ops before the arrival
+  named_bar_sync(bar_id, 128);
+  if (issuer) {
+    if (tma_reduce) bulk_wait0();   // reductions performed, not just read from smem
+    fence_proxy_async_global();
+    __threadfence();
+    if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
+    const uint32_t ticket = atom_add_acqrel_gpu_u32(counter, 1);
+    if (shared) {
+      uint32_t polls = 0;
+      while (ld_acquire_gpu_u32(counter) < S)
+        if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+    }
+    st_shared_u32(bcast, ticket);
+  }
+  named_bar_sync(bar_id, 128);
+  const uint32_t ticket = ld_shared_u32(bcast);
+  if (!shared && ticket != S - 1) return;
+  fence_proxy_async_global();
+  const int r_lo = shared ? (int)(ticket * 128 / S) : 0;
+  const int r_hi = shared ? (int)((ticket + 1) * 128 / S) : 128;
+  // coalesced pass over rows [r_lo, r_hi) of the row-major [128][kCols] tile:
+  // a warp covers 512 contiguous bytes of one row per access.
+  constexpr int kV = kCols / 4;  // float4 per tile row
+  const int n4 = (r_hi - r_lo) * kV;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+  for (int j0 = 0; j0 < n4; j0 += 128 * 16) {
+    float4 f[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int idx = j0 + row + 128 * j;
+      const int r = row0 + r_lo + idx / kV;
+      f[j] = (idx < n4 && r < args.M) ? ld_global_f4(args.ws + (size_t)r * args.L + col0 + 4 * (idx % kV)) : z;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int idx = j0 + row + 128 * j;
+      const int r = row0 + r_lo + idx / kV;
+      if (idx < n4 && r < args.M) {
+        const size_t off = (size_t)r * args.L + col0 + 4 * (idx % kV);
+        *reinterpret_cast<uint2*>(args.E + off) = make_uint2(pack_bf16x2(f[j].x, f[j].y), pack_bf16x2(f[j].z, f[j].w));
+        *reinterpret_cast<float4*>(args.ws + off) = z;
+      }
+    }
+  }
+  if (issuer) {
+    if (!shared)
+      *reinterpret_cast<volatile uint32_t*>(counter) = 0u;
+    else if (atom_add_acqrel_gpu_u32(counter, 1) == 2 * S - 1)
+      *reinterpret_cast<volatile uint32_t*>(counter) = 0u;  // every contributor is past its wait
   }
 }
 
@@ -274,7 +379,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
         pr[0] = clock64() - t_start;
         pr[1] = w_empty;
         pr[2] = w_flag;
@@ -380,7 +485,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
         pr[3] = clock64() - t_start;
         pr[4] = w_full0;
         pr[5] = w_full1;
@@ -455,10 +560,9 @@ __global__ void __launch_bounds__(256, 1)
           float w[16];
           tmem_ld16(tacc + kNB + c0, w);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (v[i] / (1.0f + __expf(-v[i]))) * w[i];
+          for (int i = 0; i < 16; ++i) v[i] = silu_fast(v[i]) * w[i];
         } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = apply_act(args.act, v[i]);
+          apply_act_frag(args.act, v);
         }
         uint32_t pk[8];
 #pragma unroll
@@ -521,11 +625,14 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
         mbar_arrive(e_empty);
+        if (args.S > 1)
+          split_finish<kLB>(args, args.tile_cnt + (u.m0 / C::BM) * (args.L / kLB) + u.l0 / kLB, tmem_slot + 8,
+                            warp == 4 && lane_id() == 0, false, u.m0, row, u.l0, 1, args.n_units <= args.n_rings);
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
     if (args.prof && warp == 4 && lane_id() == 0) {
-      unsigned long long* pr = args.prof + blockIdx.x * 16;
+      unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
       pr[9] = clock64() - t_start;
       pr[10] = w_cfull;
       pr[11] = w_ofree;
@@ -538,19 +645,6 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kTMEM_COLS>(tmem_base);
-  }
-}
-
-// fp32 workspace -> bf16 output (after the inter-cluster reduction)
-__global__ void ff_finalize_kernel(const float* __restrict__ ws, __nv_bfloat16* __restrict__ out, size_t n) {
-  size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) * 8;
-  const size_t stride = (size_t)gridDim.x * blockDim.x * 8;
-  for (; i < n; i += stride) {
-    float4 a = *reinterpret_cast<const float4*>(ws + i);
-    float4 b = *reinterpret_cast<const float4*>(ws + i + 4);
-    uint4 o = make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y),
-                         pack_bf16x2(b.z, b.w));
-    *reinterpret_cast<uint4*>(out + i) = o;
   }
 }
 

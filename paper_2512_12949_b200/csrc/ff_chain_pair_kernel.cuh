@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
+  if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;                  // ring members (pairs)
   const uint32_t q = cluster_rank();     // half of the pair (0 = leader)
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(256, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full_bar(s), 2);  // leader arrive.expect_tx + peer arrive
+      mbar_init(full_bar(s), 1);  // the leader's arrive.expect_tx covers both CTAs' bytes
       mbar_init(empty_bar(s), 1);
     }
     mbar_init(c_full, 1);
@@ -121,6 +122,7 @@ __global__ void __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+  if (threadIdx.x == 0) FF_STAMP(17);
 
   auto slot_lo = [&](int h) { return h * kblocks / G; };
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
@@ -140,11 +142,13 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
+      // Only the leader arms the (leader-owned) full barrier, for the bytes of
+      // both CTAs; the peer's loads just complete_tx on it.  A per-stage
+      // remote arrive (release.cluster) from the peer halved the TMA feed
+      // (profiles/r01/tma_variants.log: cluster-scope barrier ops 57-68 GB/s
+      // per SM vs 130 GB/s with CTA-scope ones).
       auto arm = [&]() {
-        if (leader)
-          mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
-        else
-          mbar_arrive_remote(mapa(full_bar(stage), 0));
+        if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
       };
       auto load_gemm0 = [&](int T, int kb0, int kb1) {
         const Unit u = unit_of(T / steps);
@@ -167,28 +171,39 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
       };
+      unsigned long long ready = 0;  // ring members whose C chunk of the current step is published
       auto load_hop = [&](int T, int h) {
         const Unit u = unit_of(T / steps);
         const int t = T % steps;
         const int origin = (p - h + G) % G;
         const int ncol0 = u.n0 + (t * G + origin) * C::kN0;
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
-        if (h > 0) {
-          const uint32_t* f = flag_addr(u, t, origin, (int)q);
+        if (h == 0) ready = 1ull << p;
+        if (h > 0 && !((ready >> origin) & 1ull) && !(args.dbg & 2u)) {
+          // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
-          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+          FF_TIMED(w_flag, do {
+            for (int o0 = 0; o0 < G; o0 += 8) {
+              uint32_t v[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)  // independent loads: in flight together
+                v[j] = (o0 + j < G && !((ready >> (o0 + j)) & 1ull))
+                           ? ld_relaxed_gpu_u32(flag_addr(u, t, o0 + j, (int)q))
+                           : args.epoch - 1u;
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if ((int)(v[j] - args.epoch) >= 0) ready |= 1ull << (o0 + j);
+            }
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
-          });
+          } while (!((ready >> origin) & 1ull)));
+          fence_acq_rel_gpu();
           fence_proxy_async_global();
         }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), 0);
-          if (leader)
-            mbar_expect_tx(full_bar(stage), 2 * (h > 0 ? C::kSTAGE : C::kSLOT));
-          else
-            mbar_arrive_remote(lb);
+          if (leader) mbar_expect_tx(full_bar(stage), 2 * (h > 0 ? C::kSTAGE : C::kSLOT));
           if (h > 0) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
           tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
           next();
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
         pr[0] = clock64() - t_start;
         pr[1] = w_empty;
         pr[2] = w_flag;
@@ -238,6 +253,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             const uint64_t ad = a_desc(sb, kk);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
+            if (args.dbg & 1u) continue;
             if (kGated) {
               umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
               umma_bf16_pair(tmem_base + C::kN0, ad, b_desc(sb + C::kSLOT + C::kSLOT / 2, kk), idesc0, acc);
@@ -270,8 +286,9 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t aslot = (h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
-            umma_bf16_pair(tmem_base + C::kTMEM_E, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
-                           e_started ? 1u : 0u);
+            if (!(args.dbg & 1u))
+              umma_bf16_pair(tmem_base + C::kTMEM_E, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
+                             e_started ? 1u : 0u);
             e_started = true;
           }
           umma_commit_pair(empty_bar(stage), kPairMask);
@@ -288,7 +305,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * 16;
+        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
         pr[3] = clock64() - t_start;
         pr[4] = w_full0;
         pr[5] = w_full1;
@@ -312,20 +329,20 @@ __global__ void __launch_bounds__(256, 1)
       const int t = T % steps;
       FF_TIMED(w_cfull, mbar_wait_cluster(c_full, T & 1));
       tc_fence_after();
+      if (issuer && T < 2) FF_STAMP(18 + 3 * T);
       FF_TIMED(w_ofree, mbar_wait_cluster(own_free, (T & 1) ^ 1));
       const unsigned long long t_d0 = args.prof ? clock64() : 0ull;
 #pragma unroll 1
       for (int c0 = 0; c0 < C::kCW; c0 += 32) {
         float v[32];
-        tmem_ld32(lane_base + c0, v);
         if (kGated) {
           float w[32];
-          tmem_ld32(lane_base + C::kN0 + c0, w);
+          tmem_ld32x2(lane_base + c0, lane_base + C::kN0 + c0, v, w);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = (v[i] / (1.0f + __expf(-v[i]))) * w[i];
+          for (int i = 0; i < 32; ++i) v[i] = silu_fast(v[i]) * w[i];
         } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = apply_act(args.act, v[i]);
+          tmem_ld32(lane_base + c0, v);
+          apply_act_frag(args.act, v);
         }
         uint32_t pk[16];
 #pragma unroll
@@ -348,6 +365,7 @@ __global__ void __launch_bounds__(256, 1)
       fence_proxy_async_smem();
       mbar_arrive_remote(L_own_full);
       if (args.prof) t_drain += clock64() - t_d0;
+      if (issuer && T < 2) FF_STAMP(19 + 3 * T);
       const unsigned long long t_s0 = args.prof ? clock64() : 0ull;
       if (G > 1) {
         named_bar_sync(1, 128);
@@ -364,15 +382,23 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
       if (args.prof) t_store += clock64() - t_s0;
+      if (issuer && T < 2) FF_STAMP(20 + 3 * T);
       if (t == steps - 1) {
         // E slice: TMEM -> registers -> SW128 smem tiles in the own slot -> TMA
         // store (bf16) or TMA reduce-add into the fp32 workspace (N splits).
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait_cluster(e_full, (T / steps) & 1);
         tc_fence_after();
+        if (issuer) FF_STAMP(30);
         mbar_wait_cluster(own_free, T & 1);  // own slot no longer read by hop 0 / the C store
         const int erow = u.m0 + (int)q * C::BM;
-        constexpr int kTiles = C::kCHUNK_BYTES / 16384;  // 16 KB staging tiles in the own slot
+        // Staging: the own slot (2 x 16 KB tiles), or -- for the ring's final
+        // unit, when every pipeline stage has been consumed (e_full) and no
+        // further load is coming -- the whole stage area, so the E tile leaves
+        // in one round of TMA stores / reduce-adds.
+        const bool final_unit = (T / steps) == my_units - 1;
+        const uint32_t stg = final_unit ? base : own_slot;
+        const int kTiles = final_unit ? (kStages * C::kSTAGE) / 16384 : C::kCHUNK_BYTES / 16384;
         const bool bf16_out = (args.S == 1);
         const int cols_per_tile = bf16_out ? 64 : 32;
 #pragma unroll 1
@@ -382,7 +408,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int c0 = g0; c0 < g1; c0 += 32) {
             float v[32];
             tmem_ld32(lane_base + C::kTMEM_E + c0, v);
-            const uint32_t tile = own_slot + ((c0 - g0) / cols_per_tile) * 16384;
+            const uint32_t tile = stg + ((c0 - g0) / cols_per_tile) * 16384;
             if (bf16_out) {
               uint32_t pk[16];
 #pragma unroll
@@ -402,7 +428,7 @@ __global__ void __launch_bounds__(256, 1)
           named_bar_sync(1, 128);
           if (issuer) {
             for (int c0 = g0; c0 < g1; c0 += cols_per_tile) {
-              const uint32_t tile = own_slot + ((c0 - g0) / cols_per_tile) * 16384;
+              const uint32_t tile = stg + ((c0 - g0) / cols_per_tile) * 16384;
               if (bf16_out)
                 tma_store_2d(&maps.e, tile, u.l0 + c0, erow);
               else
@@ -415,12 +441,18 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
         mbar_arrive_remote(L_e_empty);
+        if (issuer) FF_STAMP(24);
+        if (!bf16_out) {
+          split_finish<kLB>(args, args.tile_cnt + (erow / C::BM) * (args.L / kLB) + u.l0 / kLB, tmem_slot + 8, issuer,
+                            true, erow, row, u.l0, 1, args.n_units <= args.n_rings);
+          if (issuer) FF_STAMP(26);
+        }
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
     if (issuer) bulk_wait0();  // every E store / reduction performed before exit
     if (args.prof && issuer) {
-      unsigned long long* pr = args.prof + blockIdx.x * 16;
+      unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
       pr[9] = clock64() - t_start;
       pr[10] = w_cfull;
       pr[11] = w_ofree;
@@ -432,6 +464,7 @@ __global__ void __launch_bounds__(256, 1)
 
   __syncthreads();
   cluster_sync();
+  if (threadIdx.x == 0) FF_STAMP(31);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair<512>(tmem_base);

@@ -79,16 +79,21 @@ def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optiona
     return cfg
 
 
-def _workspace(nbytes: int, device):
+def _workspace(nbytes: int, device, stream):
+    """Per-(device, stream) workspace, zero-filled once when allocated.
+
+    The kernels leave it zero again (epoch-stamped flags, split counters and
+    the fp32 E region reset by the last contributor), but two launches in
+    flight at the same time must not share one, hence one per stream."""
     import torch
 
     if nbytes == 0:
         return None
-    key = (device.index if device.index is not None else torch.cuda.current_device())
+    key = (device.index if device.index is not None else torch.cuda.current_device(), int(stream.cuda_stream))
     buf = _workspaces.get(key)
     if buf is None or buf.numel() < nbytes:
-        # zero-filled once (epoch-stamped flags never need clearing again)
-        buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        with torch.cuda.stream(stream):
+            buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
         _workspaces[key] = buf
     return buf
 
@@ -115,11 +120,13 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
         out = torch.empty((d.m, d.l), dtype=torch.bfloat16, device=a.device)
     ch = chain_desc(graph)
     ws_bytes = lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(cfg))
-    ws = _workspace(ws_bytes, a.device)
+    s = stream if stream is not None else torch.cuda.current_stream(a.device)
+    if not hasattr(s, "cuda_stream"):
+        s = torch.cuda.ExternalStream(int(s), device=a.device)
+    handle = s.cuda_stream
+    ws = _workspace(ws_bytes, a.device, s)
     tp = nat.Tensors(a.data_ptr(), tensors["B0" if gated else "B"].data_ptr(),
                      tensors["B1"].data_ptr() if gated else None, tensors["D"].data_ptr(), out.data_ptr())
-    s = stream if stream is not None else torch.cuda.current_stream(a.device)
-    handle = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
     ws_ptr = ws.data_ptr() if ws is not None else None
     if c_debug is not None:
         rc = lib.ff_chain_launch_debug(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(tp), ws_ptr, ws_bytes,

@@ -6,7 +6,7 @@ names = ["prod_total","prod_w_empty","prod_w_flag","mma_total","mma_w_full_g0","
          "epi_total","epi_w_cfull","epi_w_ownfree","epi_drainC","epi_store","epi_E"]
 def prof(m,n,k,l,act,g,xchg,cfg=None):
     A,B,B1,D,E,ch,kc,ws,t = setup(m,n,k,l,act,g,cfg,xchg)
-    buf = torch.zeros(kc.grid_ctas*16 + 4096, dtype=torch.int64, device='cuda')
+    buf = torch.zeros(kc.grid_ctas*32 + 4096, dtype=torch.int64, device='cuda')
     f=lambda: nat.check(lib.ff_chain_launch(ctypes.byref(ch),ctypes.byref(kc),ctypes.byref(t),ws.data_ptr(),ws.numel(),None))
     for _ in range(3): f()
     lib.ff_set_profile_buffer(ctypes.c_void_p(buf.data_ptr()))
@@ -15,7 +15,7 @@ def prof(m,n,k,l,act,g,xchg,cfg=None):
     s=torch.cuda.Event(enable_timing=True); e=torch.cuda.Event(enable_timing=True)
     s.record(); f(); e.record(); torch.cuda.synchronize()
     ms=s.elapsed_time(e)
-    v = buf[:kc.grid_ctas*16].view(kc.grid_ctas,16).double()/1.9e3  # us at 1.9GHz
+    v = buf[:kc.grid_ctas*32].view(kc.grid_ctas,32)[:, :16].double()/1.9e3  # us at 1.9GHz
     lead = v[0::2] if xchg==2 else v
     print(f"== m{m} n{n} k{k} l{l} g{int(g)} x{xchg} {kc.as_dict()} kernel {ms*1e3:.1f}us")
     for i,nm in enumerate(names):

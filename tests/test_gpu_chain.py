@@ -199,3 +199,30 @@ def test_two_streams_and_rejections():
         bad = dict(dev)
         bad["D"] = dev["D"].t()
         runtime.run(graph, None, bad)
+
+
+@pytest.mark.parametrize("exchange,ring,splits,nb,lb", [("pair", 2, 4, 256, 256), ("l2", 2, 3, 128, 256),
+                                                        ("dsm", 2, 2, 128, 128)])
+def test_split_reduction_leaves_workspace_zero(exchange, ring, splits, nb, lb):
+    """The last of the S contributors of an E tile casts it and re-zeroes the fp32
+    tile and its arrival counter, so a workspace zero-filled once stays valid."""
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    torch = _torch()
+    m, k = 300, 256
+    l = ring * lb
+    n = splits * ring * nb * 2
+    graph = _graph("standard_ffn", "relu", m, n, k, l)
+    cfg = nat.KernelConfig()
+    cfg.ring, cfg.n_splits, cfg.nb, cfg.lb = ring, splits, nb, lb
+    cfg.exchange = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2, "pair": nat.XCHG_L2_PAIR}[exchange]
+    host, dev = _inputs("standard_ffn", m, n, k, l, seed=23)
+    for _ in range(3):
+        out = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+        assert _check("standard_ffn", "relu", host, out) <= TOL
+    stream = torch.cuda.current_stream()
+    ws = runtime._workspaces[(torch.cuda.current_device(), int(stream.cuda_stream))]
+    lo, hi = 1 << 20, (1 << 20) + (256 << 10) + m * l * 4
+    assert int(ws[lo:hi].count_nonzero()) == 0
