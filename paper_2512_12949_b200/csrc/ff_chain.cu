@@ -134,7 +134,9 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   WsLayout w{};
   const bool pair = c->exchange == FF_XCHG_L2_PAIR;
   const size_t e_bytes = c->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
-  const bool c_scratch = c->exchange != FF_XCHG_DSM && c->ring > 1;
+  // C scratch: L2 transport with a ring > 1; the standard-FFN pair kernel also
+  // reads its own chunk back from it (hop 0), so it always needs one.
+  const bool c_scratch = c->exchange != FF_XCHG_DSM && (c->ring > 1 || (pair && ch->kind != FF_KIND_GATED));
   w.f_off = 0;
   w.n_off = kFlagBytes;
   w.e_off = kFlagBytes + kCntBytes;
@@ -292,7 +294,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     ok = ok && make_map_nd(&maps.d, BF, 3, t->d, d, st, b);
   }
   {  // C scratch [mpad][N] as {64, mpad, N/64}
-    const bool l2x = cfg->ring > 1;
+    const bool l2x = cfg->ring > 1 || !kGated;
     const uint64_t d[3] = {64, l2x ? mpad : M, l2x ? N / 64 : K / 64}, st[2] = {(l2x ? N : K) * 2, 128};
     const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.c, BF, 3, l2x ? (const void*)(wsb + wl.c_off) : t->a, d, st, b);
@@ -351,7 +353,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   attr[1].id = cudaLaunchAttributeCooperative;
   attr[1].val.cooperative = 1;
   lc.attrs = attr;
-  lc.numAttrs = 2;
+  lc.numAttrs = (g_dbg & 4u) ? 1 : 2;  // diagnostics bit2: plain cluster launch
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, a);
   if (e != cudaSuccess) {
     // cooperative + cluster not accepted: the grid is sized to co-residency anyway

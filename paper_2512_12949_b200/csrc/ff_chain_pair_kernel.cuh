@@ -44,8 +44,15 @@ struct PairCfg {
   static constexpr int kSLOT = 32768;             // one operand tile (A or B / C or D) per stage
   static constexpr int kSTAGE = 2 * kSLOT;
   static constexpr int kCHUNK_BYTES = BM * kCW * 2;  // own C chunk (bf16, K-major SW128 64-col tiles)
+  // The own slot (32 KB) stages the drained C chunk for its TMA store (in
+  // 128-column rounds) and E tiles.  When the whole chunk fits (gated, 128
+  // columns) hop 0 also reads it from there as the MMA A operand; otherwise
+  // hop 0 loads the own chunk back from L2 like every other hop, which keeps a
+  // third 64 KB pipeline stage for the standard FFN.
+  static constexpr int kOWN_BYTES = 32768;
+  static constexpr bool kOwnFull = kCHUNK_BYTES <= kOWN_BYTES;
   static constexpr int kOFF_OWN = kStages * kSTAGE;
-  static constexpr int kOFF_BAR = kOFF_OWN + kCHUNK_BYTES;
+  static constexpr int kOFF_BAR = kOFF_OWN + kOWN_BYTES;
   static constexpr int kNUM_BARS = 2 * kStages + 8;
   static constexpr int kSMEM = kOFF_BAR + kNUM_BARS * 8 + 16 + 1024;
   static constexpr int kTMEM_E = 256;
@@ -105,7 +112,8 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(c_full, 1);
     mbar_init(c_empty, 256);  // both CTAs' epilogues arrive on the leader's barrier
     mbar_init(own_full, 256);
-    mbar_init(own_free, G > 1 ? 2 : 1);
+    // own slot free again after: the C store read it (+ the MMA's hop 0 when it is the A operand)
+    mbar_init(own_free, (C::kOwnFull && G > 1) ? 2 : 1);
     mbar_init(e_full, 1);
     mbar_init(e_empty, 256);
     fence_mbar_init();
@@ -115,7 +123,7 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&maps.b);
     if (kGated && !kPackedB) tma_prefetch_desc(&maps.b1);
     tma_prefetch_desc(&maps.d);
-    if (G > 1) tma_prefetch_desc(&maps.c);
+    if (G > 1 || !C::kOwnFull) tma_prefetch_desc(&maps.c);
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
   tc_fence_before();
@@ -178,8 +186,9 @@ __global__ void __launch_bounds__(256, 1)
         const int origin = (p - h + G) % G;
         const int ncol0 = u.n0 + (t * G + origin) * C::kN0;
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
-        if (h == 0) ready = 1ull << p;
-        if (h > 0 && !((ready >> origin) & 1ull) && !(args.dbg & 2u)) {
+        const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
+        if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
+        if (from_l2 && !((ready >> origin) & 1ull) && !(args.dbg & 2u)) {
           // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
           FF_TIMED(w_flag, do {
@@ -203,8 +212,8 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), 0);
-          if (leader) mbar_expect_tx(full_bar(stage), 2 * (h > 0 ? C::kSTAGE : C::kSLOT));
-          if (h > 0) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
+          if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
+          if (from_l2) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
           tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
           next();
         }
@@ -277,13 +286,13 @@ __global__ void __launch_bounds__(256, 1)
           }
           e_started = false;
         }
-        if (h == 0) FF_TIMED(w_own, mbar_wait_cluster(own_full, T & 1));
+        if (C::kOwnFull && h == 0) FF_TIMED(w_own, mbar_wait_cluster(own_full, T & 1));
         tc_fence_after();
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t aslot = (h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
+          const uint32_t aslot = (C::kOwnFull && h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             if (!(args.dbg & 1u))
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(256, 1)
           umma_commit_pair(empty_bar(stage), kPairMask);
           next();
         }
-        if (h == 0) umma_commit_pair(own_free, kPairMask);
+        if (C::kOwnFull && h == 0) umma_commit_pair(own_free, kPairMask);
         if (t == steps - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
       };
       if (total_steps > 0) gemm0(0, 0, kblocks);
@@ -332,54 +341,65 @@ __global__ void __launch_bounds__(256, 1)
       if (issuer && T < 2) FF_STAMP(18 + 3 * T);
       FF_TIMED(w_ofree, mbar_wait_cluster(own_free, (T & 1) ^ 1));
       const unsigned long long t_d0 = args.prof ? clock64() : 0ull;
+      const bool publish = G > 1 || !C::kOwnFull;  // the chunk goes to the L2 scratch
+      const int nblk = (u.n0 + (t * G + p) * C::kN0) / 64;
+      constexpr int kRoundCols = C::kOWN_BYTES / (C::BM * 2);  // 128 columns per own-slot round
 #pragma unroll 1
-      for (int c0 = 0; c0 < C::kCW; c0 += 32) {
-        float v[32];
-        if (kGated) {
-          float w[32];
-          tmem_ld32x2(lane_base + c0, lane_base + C::kN0 + c0, v, w);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = silu_fast(v[i]) * w[i];
-        } else {
-          tmem_ld32(lane_base + c0, v);
-          apply_act_frag(args.act, v);
+      for (int r0 = 0; r0 < C::kCW; r0 += kRoundCols) {
+        if (r0 > 0) {  // the previous round's TMA store must have read the own slot
+          if (issuer) bulk_wait_read0();
+          named_bar_sync(1, 128);
         }
-        uint32_t pk[16];
+#pragma unroll 1
+        for (int c0 = r0; c0 < r0 + kRoundCols; c0 += 32) {
+          float v[32];
+          if (kGated) {
+            float w[32];
+            tmem_ld32x2(lane_base + c0, lane_base + C::kN0 + c0, v, w);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-        const uint32_t tile = own_slot + (c0 / 64) * 16384;
-        const int ch = (c0 % 64) / 8;
+            for (int i = 0; i < 32; ++i) v[i] = silu_fast(v[i]) * w[i];
+          } else {
+            tmem_ld32(lane_base + c0, v);
+            apply_act_frag(args.act, v);
+          }
+          uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-        const int grow = u.m0 + (int)q * C::BM + row;
-        if (args.c_debug != nullptr && grow < args.M) {
-          const int ncol = u.n0 + (t * G + p) * C::kN0 + c0;
-          uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)grow * args.N + ncol);
+          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+          const uint32_t tile = own_slot + ((c0 - r0) / 64) * 16384;
+          const int ch = (c0 % 64) / 8;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          for (int j = 0; j < 4; ++j)
+            st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          const int grow = u.m0 + (int)q * C::BM + row;
+          if (args.c_debug != nullptr && grow < args.M) {
+            const int ncol = u.n0 + (t * G + p) * C::kN0 + c0;
+            uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)grow * args.N + ncol);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+        if (r0 + kRoundCols >= C::kCW) {  // C accumulator fully read: GEMM0 of the next step may start
+          tc_fence_before();
+          mbar_arrive_remote(L_c_empty);
+        }
+        fence_proxy_async_smem();
+        if (C::kOwnFull) mbar_arrive_remote(L_own_full);
+        if (publish) {
+          named_bar_sync(1, 128);
+          if (issuer) {
+            tma_store_3d(&maps.c, own_slot, 0, u.m0 + (int)q * C::BM, nblk + r0 / 64);
+            bulk_commit();
+          }
         }
       }
-      tc_fence_before();
-      mbar_arrive_remote(L_c_empty);
-      fence_proxy_async_smem();
-      mbar_arrive_remote(L_own_full);
       if (args.prof) t_drain += clock64() - t_d0;
       if (issuer && T < 2) FF_STAMP(19 + 3 * T);
       const unsigned long long t_s0 = args.prof ? clock64() : 0ull;
-      if (G > 1) {
-        named_bar_sync(1, 128);
-        if (issuer) {
-          const int nblk = (u.n0 + (t * G + p) * C::kN0) / 64;
-#pragma unroll
-          for (int j = 0; j < C::kCW / 128; ++j)
-            tma_store_3d(&maps.c, own_slot + j * 32768, 0, u.m0 + (int)q * C::BM, nblk + 2 * j);
-          bulk_commit();
-          bulk_wait0();
-          fence_proxy_async_global();
-          st_release_gpu_u32(flag_addr(u, t, p, (int)q), args.epoch);
-          mbar_arrive(own_free);
-        }
+      if (publish && issuer) {
+        bulk_wait0();
+        fence_proxy_async_global();
+        st_release_gpu_u32(flag_addr(u, t, p, (int)q), args.epoch);
+        mbar_arrive(own_free);
       }
       if (args.prof) t_store += clock64() - t_s0;
       if (issuer && T < 2) FF_STAMP(20 + 3 * T);
@@ -398,7 +418,7 @@ __global__ void __launch_bounds__(256, 1)
         // in one round of TMA stores / reduce-adds.
         const bool final_unit = (T / steps) == my_units - 1;
         const uint32_t stg = final_unit ? base : own_slot;
-        const int kTiles = final_unit ? (kStages * C::kSTAGE) / 16384 : C::kCHUNK_BYTES / 16384;
+        const int kTiles = final_unit ? (kStages * C::kSTAGE) / 16384 : C::kOWN_BYTES / 16384;
         const bool bf16_out = (args.S == 1);
         const int cols_per_tile = bf16_out ? 64 : 32;
 #pragma unroll 1
