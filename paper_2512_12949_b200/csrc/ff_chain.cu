@@ -115,7 +115,7 @@ int table_active_clusters(int cluster, int num_sms) {
 }
 
 struct WsLayout {
-  size_t e_off, c_off, f_off, n_off, total;
+  size_t e_off, c_off, f_off, n_off, s_off, total;
   bool e_memset;  // fp32 E larger than the zero zone: clear it before the launch
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -145,6 +145,9 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   if (c_scratch) off = w.e_off + std::max(e_bytes, kEZoneBytes);
   w.c_off = off;
   if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
+  // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
+  w.s_off = off;
+  if (pair && c->n_splits > 1) off = align256(off + (size_t)c->n_splits * ch->m * ch->l * sizeof(float));
   w.total = off;
   return w;
 }
@@ -310,6 +313,22 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     ok = ok && make_map_nd(&maps.w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, cfg->n_splits > 1 ? (const void*)(wsb + wl.e_off) : t->e,
                            d, st, b);
   }
+  {  // whole-tile / row-slice 3D views of E and the fp32 workspace (final-unit epilogue)
+    const uint32_t rs = 128u / (uint32_t)std::max(1, cfg->n_splits);  // split row slice
+    const uint64_t de[3] = {64, M, L / 64}, se[2] = {L * 2, 128};
+    const uint32_t be[3] = {64, 128, 256 / 64}, ber[3] = {64, rs, 256 / 64};
+    ok = ok && make_map_nd(&maps.e3, BF, 3, t->e, de, se, be);
+    ok = ok && make_map_nd(&maps.er, BF, 3, t->e, de, se, ber);
+    const void* wp = cfg->n_splits > 1 ? (const void*)(wsb + wl.e_off) : t->e;
+    const uint64_t dw[3] = {32, M, L / 32}, sw[2] = {L * 4, 128};
+    const uint32_t bw[3] = {32, 128, 256 / 32};
+    ok = ok && make_map_nd(&maps.w3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, wp, dw, sw, bw);
+    const uint64_t S = (uint64_t)std::max(1, cfg->n_splits);
+    const void* sp = cfg->n_splits > 1 ? (const void*)(wsb + wl.s_off) : t->e;
+    const uint64_t ds[4] = {32, M, S, L / 32}, ss[3] = {L * 4, M * L * 4, 128};
+    const uint32_t bs[4] = {32, rs, 1, 256 / 32};
+    ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, sp, ds, ss, bs);
+  }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   if (cfg->ring > 64) return fail(FF_ERR_UNSUPPORTED, "ring of more than 64 pairs");
@@ -336,6 +355,16 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
+  // hops deferred past GEMM0(T+1): about one C drain (+ its store for the
+  // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
+  a.defer = cfg->ring - 1 - cfg->ring / 4;  // measured: 3/4 of the hops (profiles/r01/cfgs_defer.log)
+  // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
+  a.finish_tma = cfg->n_splits > 1 && cfg->n_splits <= 16 && cfg->units <= rings && 128 % cfg->n_splits == 0 &&
+                 (128 / cfg->n_splits) % 8 == 0 &&
+                 (size_t)((M + 255) / 256) * 2 * (L / 256) * 16 <= (1u << 17);
+  if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);
+  a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
+  if ((g_dbg >> 12) & 15u) a.prefetch = (int)((g_dbg >> 12) & 15u) - 1;
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
@@ -593,8 +622,10 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   if (rc) return rc;
   const size_t need = ws_layout(ch, &cfg).total;
   if (need && (ws == nullptr || ws_bytes < need)) return fail(FF_ERR_ARG, "workspace too small");
+  // L2 ready flags live in the lower half of the flag region (the pair
+  // kernel's split slab flags use the upper half)
   if (cfg.exchange != FF_XCHG_DSM &&
-      (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes)
+      (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes / 2)
     return fail(FF_ERR_UNSUPPORTED, "too many (unit, step, member) chunks for the flag region");
   if (cfg.n_splits > 1 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / cfg.lb) * sizeof(uint32_t) > kCntBytes)
     return fail(FF_ERR_UNSUPPORTED, "too many E tiles for the split arrival counters");

@@ -33,6 +33,11 @@ struct PairMaps {
   CUtensorMap c;    // C scratch [Mpad][N]: 3D {64, Mpad, N/64}, box {64, 128, 2}
   CUtensorMap e;    // E [M][L] bf16: 2D box {64, 128}
   CUtensorMap w;    // fp32 workspace [M][L]: 2D box {32, 128}
+  // single-instruction E tiles for a ring's final unit (stage area as staging):
+  CUtensorMap e3;   // E bf16 3D {64, M, L/64}, box {64, 128, kLB/64}
+  CUtensorMap w3;   // fp32 workspace 3D {32, M, L/32}, box {32, 128, kLB/32}
+  CUtensorMap er;   // E bf16 3D, box {64, 128/S, kLB/64}: one row slice of a tile
+  CUtensorMap slab; // fp32 split partials 4D {32, M, S, L/32}, box {32, 128/S, 1, kLB/32}
 };
 
 template <bool kGated, int kLB, int kStages>
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(256, 1)
   const int total_steps = my_units * steps;
 
   struct Unit {
-    int m0, l0, n0, id;
+    int m0, l0, n0, id, split;
   };
   auto unit_of = [&](int i) {
     const int u = ring + i * args.n_rings;
@@ -91,7 +96,7 @@ __global__ void __launch_bounds__(256, 1)
     const int rest = u / args.m_tiles;
     const int lc = rest % args.l_clusters;
     const int split = rest / args.l_clusters;
-    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * steps * G * C::kN0, u};
+    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * steps * G * C::kN0, u, split};
   };
 
   const uint32_t bar0 = base + C::kOFF_BAR;
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(256, 1)
   auto empty_bar = [&](int s) { return bar0 + 8u * (kStages + s); };
   const uint32_t bx = bar0 + 8u * (2 * kStages);
   const uint32_t c_full = bx, c_empty = bx + 8, own_full = bx + 16, own_free = bx + 24;
-  const uint32_t e_full = bx + 32, e_empty = bx + 40;
+  const uint32_t e_full = bx + 32, e_empty = bx + 40, e_load = bx + 48;
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
   const uint32_t own_slot = base + C::kOFF_OWN;
   constexpr uint16_t kPairMask = 0x3;
@@ -116,6 +121,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(own_free, (C::kOwnFull && G > 1) ? 2 : 1);
     mbar_init(e_full, 1);
     mbar_init(e_empty, 256);
+    mbar_init(e_load, 1);
     fence_mbar_init();
   }
   if (warp == 0 && elect_one()) {
@@ -132,7 +138,11 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
   if (threadIdx.x == 0) FF_STAMP(17);
 
-  auto slot_lo = [&](int h) { return h * kblocks / G; };
+  // GEMM0 of step T+1 is spread over the first G - defer hops of step T; the
+  // last `defer` hops run after it, while the epilogue drains C(T+1), so the
+  // tensor core does not idle through the drain.
+  const int g0_slices = G - args.defer;
+  auto slot_lo = [&](int h) { return h < g0_slices ? h * kblocks / g0_slices : kblocks; };
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
   };
@@ -159,6 +169,7 @@ __global__ void __launch_bounds__(256, 1)
         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
       };
       auto load_gemm0 = [&](int T, int kb0, int kb1) {
+        if (kb0 >= kb1) return;
         const Unit u = unit_of(T / steps);
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
         const int nblk = (u.n0 + ((T % steps) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
@@ -168,6 +179,15 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t lb = mapa(full_bar(stage), 0);
           arm();
           tma_load_3d_pair(sb, &maps.a, lb, 0, u.m0 + (int)q * C::BM, kb * (C::BK / 64));
+          // L2 prefetch of the B tile `prefetch` k-blocks ahead: the weights
+          // stream from HBM; the extra lead hides its latency behind 3 stages
+          const int pf = args.prefetch;
+          if (pf && kb + pf < kblocks) {
+            if (!kGated || !kPackedB)
+              tma_prefetch_l2_3d(&maps.b, 0, (kb + pf) * C::BK, nblk);
+            else
+              tma_prefetch_l2_4d(&maps.b, 0, (kb + pf) * C::BK, nblk, 0);
+          }
           if (!kGated) {
             tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
           } else if (kPackedB) {
@@ -207,6 +227,10 @@ __global__ void __launch_bounds__(256, 1)
           } while (!((ready >> origin) & 1ull)));
           fence_acq_rel_gpu();
           fence_proxy_async_global();
+        }
+        if (args.prefetch && h + args.prefetch < G) {  // D rows of a later hop of this step
+          const int ncol_pf = u.n0 + (t * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
+          for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) tma_prefetch_l2_3d(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk);
         }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
@@ -250,6 +274,7 @@ __global__ void __launch_bounds__(256, 1)
       auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
       auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
       auto gemm0 = [&](int T, int kb0, int kb1) {
+        if (kb0 >= kb1) return;
         if (kb0 == 0) {
           FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, (T & 1) ^ 1));
           tc_fence_after();
@@ -333,6 +358,69 @@ __global__ void __launch_bounds__(256, 1)
     const unsigned long long t_start = clock64();
     // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
     auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
+    // Split-N reduce-scatter for a ring's final unit when every unit is some
+    // ring's final one (no wait can then block another unit).  The fp32 E
+    // partial is staged slice-major -- [S slices][kLB/32 col groups][R rows][128 B],
+    // R = 128/S -- so split s keeps slice s in shared memory, TMA-stores every
+    // other slice j into its slab (j's row slice of split s's partial), flags it,
+    // then loads the S-1 partner slices of slice s, sums the S partials in split
+    // order (deterministic) and TMA-stores bf16 E rows [s*R, s*R+R).  Plain
+    // bulk stores and loads only: no atomics, nothing to re-zero.
+    auto slab_flag = [&](int tile, int s_) { return args.flags + (1u << 17) + tile * 16 + s_; };
+    auto split_reduce_scatter = [&](const Unit& u, int row0) {
+      const int S = args.S, R = C::BM / S, sp = u.split;
+      const int tile = (row0 / C::BM) * (args.L / kLB) + u.l0 / kLB;
+      if (issuer) {
+        for (int j = 0; j < S; ++j)
+          if (j != sp) tma_store_4d(&maps.slab, base + j * (R * 1024), 0, row0 + j * R, sp, u.l0 / 32);
+        bulk_commit();
+        bulk_wait0();  // slices written to the slab
+        fence_proxy_async_global();
+        st_release_gpu_u32(slab_flag(tile, sp), args.epoch);
+        if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
+        // partners' slices of this row slice
+        uint32_t polls = 0;
+        for (int j = 0; j < S; ++j) {
+          if (j == sp) continue;
+          while ((int)(ld_relaxed_gpu_u32(slab_flag(tile, j)) - args.epoch) < 0)
+            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+        }
+        fence_acq_rel_gpu();
+        fence_proxy_async_global();
+        if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 27] = globaltimer_ns();
+        mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kLB * 4));
+        for (int j = 0; j < S; ++j)
+          if (j != sp) tma_load_4d(base + j * (R * 1024), &maps.slab, e_load, 0, row0 + sp * R, j, u.l0 / 32);
+      }
+      mbar_wait(e_load, 0);
+      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 28] = globaltimer_ns();
+      // sum in split order, cast, stage bf16 [kLB/64][R][128 B] after the fp32 area
+      const uint32_t ebuf_off = C::BM * kLB * 4;
+      const uint8_t* const src = smem_gen;
+#pragma unroll 4
+      for (int it = row; it < R * (kLB / 4); it += 128) {
+        const int r = it / (kLB / 4), c16 = it % (kLB / 4);
+        const uint32_t off = (c16 / 8) * (R * 128) + r * 128 + (((c16 % 8) ^ (r & 7)) << 4);
+        float4 acc = *reinterpret_cast<const float4*>(src + off);
+        for (int j = 1; j < S; ++j) {
+          const float4 f = *reinterpret_cast<const float4*>(src + j * (R * 1024) + off);
+          acc.x += f.x;
+          acc.y += f.y;
+          acc.z += f.z;
+          acc.w += f.w;
+        }
+        const int ch = (c16 % 16) / 2;
+        *reinterpret_cast<uint2*>(smem_gen + ebuf_off + (c16 / 16) * (R * 128) + r * 128 + ((ch ^ (r & 7)) << 4) +
+                                  (c16 & 1) * 8) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+      }
+      const uint32_t ebuf = base + ebuf_off;
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (issuer) {
+        tma_store_3d(&maps.er, ebuf, 0, row0 + sp * R, u.l0 / 64);
+        bulk_commit();
+      }
+    };
     for (int T = 0; T < total_steps; ++T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
@@ -421,6 +509,73 @@ __global__ void __launch_bounds__(256, 1)
         const int kTiles = final_unit ? (kStages * C::kSTAGE) / 16384 : C::kOWN_BYTES / 16384;
         const bool bf16_out = (args.S == 1);
         const int cols_per_tile = bf16_out ? 64 : 32;
+        uint32_t* const tile_counter = args.tile_cnt + (erow / C::BM) * (args.L / kLB) + u.l0 / kLB;
+        if (final_unit) {
+          // whole E tile staged at once: [kLB/cols_per_tile][128 rows][128 B] SW128 tiles, one TMA instruction
+#pragma unroll 1
+          const bool scatter = !bf16_out && args.finish_tma;
+          if (scatter) {
+            // slice-major staging: row -> (slice, row in slice); two TMEM loads per wait
+            const int R = C::BM / args.S;
+            const int rr = row % R;
+            float4* const rbase = reinterpret_cast<float4*>(smem_gen + (row / R) * (R * 1024) + rr * 128);
+#pragma unroll 1
+            for (int c0 = 0; c0 < kLB; c0 += 64) {
+              float v[32], w[32];
+              tmem_ld32x2(lane_base + C::kTMEM_E + c0, lane_base + C::kTMEM_E + c0 + 32, v, w);
+              float4* const d0 = rbase + (c0 / 32) * (R * 8);
+              float4* const d1 = d0 + R * 8;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                d0[j ^ (rr & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                d1[j ^ (rr & 7)] = make_float4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+              }
+            }
+          }
+          for (int c0 = 0; c0 < (scatter ? 0 : kLB); c0 += 32) {
+            float v[32];
+            tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+            const uint32_t tile = base + (c0 / cols_per_tile) * 16384;
+            if (bf16_out) {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              const int ch = (c0 % 64) / 8;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                st_shared_v4(swz(tile, j), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            }
+          }
+          tc_fence_before();
+          mbar_arrive_remote(L_e_empty);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (scatter) {
+            if (issuer) FF_STAMP(24);
+            split_reduce_scatter(u, erow);
+            if (issuer) FF_STAMP(26);
+          } else if (issuer) {
+            if (bf16_out)
+              tma_store_3d(&maps.e3, base, 0, erow, u.l0 / 64);
+            else if (args.dbg & 8u)  // diagnostics: plain store instead of reduce-add (wrong sums)
+              tma_store_3d(&maps.w3, base, 0, erow, u.l0 / 32);
+            else if (args.dbg & 16u)  // diagnostics: eight 16 KB reduce-adds instead of one 128 KB
+              for (int c = 0; c < kLB / 32; ++c) tma_reduce_add_2d(&maps.w, base + c * 16384, u.l0 + 32 * c, erow);
+            else
+              tma_reduce_add_3d(&maps.w3, base, 0, erow, u.l0 / 32);
+            bulk_commit();
+            FF_STAMP(24);
+          }
+          if (!bf16_out && !scatter) {
+            split_finish<kLB>(args, tile_counter, tmem_slot + 8, issuer, true, erow, row, u.l0, 1, false);
+            if (issuer) FF_STAMP(26);
+          }
+        } else {
 #pragma unroll 1
         for (int g0 = 0; g0 < kLB; g0 += cols_per_tile * kTiles) {
           const int g1 = (g0 + cols_per_tile * kTiles < kLB) ? g0 + cols_per_tile * kTiles : kLB;
@@ -463,9 +618,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive_remote(L_e_empty);
         if (issuer) FF_STAMP(24);
         if (!bf16_out) {
-          split_finish<kLB>(args, args.tile_cnt + (erow / C::BM) * (args.L / kLB) + u.l0 / kLB, tmem_slot + 8, issuer,
-                            true, erow, row, u.l0, 1, args.n_units <= args.n_rings);
+          split_finish<kLB>(args, tile_counter, tmem_slot + 8, issuer, true, erow, row, u.l0, 1, false);
           if (issuer) FF_STAMP(26);
+        }
         }
         if (args.prof) t_e += clock64() - t_e0;
       }

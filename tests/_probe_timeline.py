@@ -33,7 +33,7 @@ def timeline(m,n,k,l,act,g,xchg,cfg=None):
     rel = (tl - t0)/1e3
     rel[tl==0] = float('nan')
     print(f"== m{m} n{n} k{k} l{l} g{int(g)} x{xchg} {kc.as_dict()} events {ms_plain*1e3:.1f}us (profiled {ms*1e3:.1f}us)")
-    names = {0:'entry',1:'setup',8:'E_reduced',9:'E_ticket',10:'E_finished',14:'E_start',15:'exit'}
+    names = {0:'entry',1:'setup',8:'E_staged',9:'E_slabs_out',10:'E_finished',11:'E_flags_in',12:'E_loaded',14:'E_start',15:'exit'}
     for T in range(2):
         names[2+3*T]=f'cfull{T}'; names[3+3*T]=f'drained{T}'; names[4+3*T]=f'stored{T}'
     for i in range(16):
