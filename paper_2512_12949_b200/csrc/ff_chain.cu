@@ -382,7 +382,11 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   attr[1].id = cudaLaunchAttributeCooperative;
   attr[1].val.cooperative = 1;
   lc.attrs = attr;
-  lc.numAttrs = (g_dbg & 4u) ? 1 : 2;  // diagnostics bit2: plain cluster launch
+  // Cooperative + cluster guarantees co-residency of the rings; ncu cannot
+  // replay that combination, so FF_NO_COOPERATIVE=1 (profiling) or debug bit2
+  // drops the cooperative attribute (the grid is sized to fit either way).
+  static const bool no_coop = std::getenv("FF_NO_COOPERATIVE") != nullptr;
+  lc.numAttrs = ((g_dbg & 4u) || no_coop) ? 1 : 2;
   cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, a);
   if (e != cudaSuccess) {
     // cooperative + cluster not accepted: the grid is sized to co-residency anyway

@@ -397,23 +397,46 @@ __global__ void __launch_bounds__(256, 1)
       // sum in split order, cast, stage bf16 [kLB/64][R][128 B] after the fp32 area
       const uint32_t ebuf_off = C::BM * kLB * 4;
       const uint8_t* const src = smem_gen;
-#pragma unroll 4
-      for (int it = row; it < R * (kLB / 4); it += 128) {
-        const int r = it / (kLB / 4), c16 = it % (kLB / 4);
-        const uint32_t off = (c16 / 8) * (R * 128) + r * 128 + (((c16 % 8) ^ (r & 7)) << 4);
-        float4 acc = *reinterpret_cast<const float4*>(src + off);
-        for (int j = 1; j < S; ++j) {
-          const float4 f = *reinterpret_cast<const float4*>(src + j * (R * 1024) + off);
-          acc.x += f.x;
-          acc.y += f.y;
-          acc.z += f.z;
-          acc.w += f.w;
+      const int n_items = (args.dbg & 32u) ? 0 : R * (kLB / 4);  // diagnostics: skip the sum
+      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 29] = globaltimer_ns();
+      // four independent items per thread in flight (loads first, then adds)
+      __syncwarp();
+#pragma unroll 1
+      for (int it0 = row; it0 < n_items; it0 += 512) {
+        uint32_t off[4];
+        float4 acc[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int it = it0 + 128 * q4;
+          const int r = it / (kLB / 4), c16 = it % (kLB / 4);
+          off[q4] = (c16 / 8) * (R * 128) + r * 128 + (((c16 % 8) ^ (r & 7)) << 4);
+          acc[q4] = *reinterpret_cast<const float4*>(src + off[q4]);
         }
-        const int ch = (c16 % 16) / 2;
-        *reinterpret_cast<uint2*>(smem_gen + ebuf_off + (c16 / 16) * (R * 128) + r * 128 + ((ch ^ (r & 7)) << 4) +
-                                  (c16 & 1) * 8) = make_uint2(pack_bf16x2(acc.x, acc.y), pack_bf16x2(acc.z, acc.w));
+#pragma unroll 1
+        for (int j = 1; j < S; ++j) {
+          float4 f[4];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) f[q4] = *reinterpret_cast<const float4*>(src + j * (R * 1024) + off[q4]);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            acc[q4].x += f[q4].x;
+            acc[q4].y += f[q4].y;
+            acc[q4].z += f[q4].z;
+            acc[q4].w += f[q4].w;
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int it = it0 + 128 * q4;
+          const int r = it / (kLB / 4), c16 = it % (kLB / 4);
+          const int ch = (c16 % 16) / 2;
+          *reinterpret_cast<uint2*>(smem_gen + ebuf_off + (c16 / 16) * (R * 128) + r * 128 + ((ch ^ (r & 7)) << 4) +
+                                    (c16 & 1) * 8) =
+              make_uint2(pack_bf16x2(acc[q4].x, acc[q4].y), pack_bf16x2(acc[q4].z, acc[q4].w));
+        }
       }
       const uint32_t ebuf = base + ebuf_off;
+      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 22] = globaltimer_ns();
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (issuer) {

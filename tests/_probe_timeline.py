@@ -33,13 +33,13 @@ def timeline(m,n,k,l,act,g,xchg,cfg=None):
     rel = (tl - t0)/1e3
     rel[tl==0] = float('nan')
     print(f"== m{m} n{n} k{k} l{l} g{int(g)} x{xchg} {kc.as_dict()} events {ms_plain*1e3:.1f}us (profiled {ms*1e3:.1f}us)")
-    names = {0:'entry',1:'setup',8:'E_staged',9:'E_slabs_out',10:'E_finished',11:'E_flags_in',12:'E_loaded',14:'E_start',15:'exit'}
-    for T in range(2):
+    names = {0:'entry',1:'setup',6:'E_summed',8:'E_staged',9:'E_slabs_out',10:'E_finished',11:'E_flags_in',12:'E_loaded',13:'E_sum0',14:'E_start',15:'exit'}
+    for T in range(1):
         names[2+3*T]=f'cfull{T}'; names[3+3*T]=f'drained{T}'; names[4+3*T]=f'stored{T}'
     for i in range(16):
         col = rel[:,i]; col = col[~torch.isnan(col)]
         if col.numel()==0: continue
-        print(f"   {names.get(i,i):10s} min {col.min().item():7.1f} mean {col.mean().item():7.1f} max {col.max().item():7.1f} us")
+        print(f"   {str(names.get(i,i)):10s} min {col.min().item():7.1f} mean {col.mean().item():7.1f} max {col.max().item():7.1f} us")
 def cublas(m,n,k,l,g):
     A=torch.randn(m,k,device='cuda').bfloat16(); B=torch.randn(k,(2 if g else 1)*n,device='cuda').bfloat16()
     C=torch.randn(m,n,device='cuda').bfloat16(); D=torch.randn(n,l,device='cuda').bfloat16()

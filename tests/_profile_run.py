@@ -8,7 +8,7 @@ for name in names:
     kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
     t = bench.make_device_inputs(kind, m, n, k, l, 3, "cuda")
     g = bench.graph_of(name)
-    cfg = runtime.lower(g, None, 148, "l2")
+    cfg = runtime.lower(g, None, 148, sys.argv[0] and "pair")
     out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     for i in range(3):
