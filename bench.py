@@ -73,34 +73,81 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    polled every 5 ms from a thread (nvidia-smi -lms as a fallback)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []
+        self.stop_evt = threading.Event()
+        self.thread = None
+        self.nvml = None
         self.proc = None
         self.lines = []
-        self.thread = None
+
+    def _handle(self, pynvml):
+        try:
+            import torch
+
+            bus = "%04x:%02x:%02x.0" % (torch.cuda.get_device_properties(self.index).pci_domain_id,
+                                         torch.cuda.get_device_properties(self.index).pci_bus_id,
+                                         torch.cuda.get_device_properties(self.index).pci_device_id)
+            return pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (FileNotFoundError, OSError):
-            self.proc = None
-            return
-        self.thread = threading.Thread(target=self._pump, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = self._handle(pynvml)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = (pynvml, h)
+        except Exception:
+            self.nvml = None
+        if self.nvml is None:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except (FileNotFoundError, OSError):
+                self.proc = None
+                return
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+        else:
+            self.thread = threading.Thread(target=self._poll, daemon=True)
         self.thread.start()
+
+    def _poll(self):
+        pynvml, h = self.nvml
+        while not self.stop_evt.is_set():
+            try:
+                mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(mhz), int(bits)))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def _pump(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self) -> dict:
+        if self.nvml is not None:
+            self.stop_evt.set()
+            self.thread.join(timeout=2)
+            sm = [m for m, _ in self.samples]
+            reasons = sorted({name for _, b in self.samples for bit, name in self.REASONS.items() if b & bit})
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                    "reasons": reasons, "samples": len(sm), "source": "nvml 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -124,7 +171,7 @@ class ClockSampler:
                 if val.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 100 ms"}
 
 
 # ----------------------------------------------------------------------------- CPU baseline
@@ -429,17 +476,27 @@ def run_reference(args, rank, world):
     kind, act, m, n, k, l, desc = WORKLOADS[args.workload]
     import oracle
 
-    plan_doc = _rows_plan(_reference_plan(args.workload), m)
-    inputs = oracle.make_inputs(kind, m, n, k, l, seed=0, dtype=np.float32)
+    # each step = one plan-faithful replay of a token-row sample of the chain,
+    # sized so the whole --steps K --warmup W run stays within ~2 minutes
+    plan_full = _reference_plan(args.workload)
+    probe_rows = min(m, 64)
+    probe_in = oracle.make_inputs(kind, probe_rows, n, k, l, seed=0, dtype=np.float32)
+    t0 = time.perf_counter()
+    cpu_reference_step(kind, act, probe_rows, n, k, l, probe_in, _rows_plan(plan_full, probe_rows))
+    per_row = (time.perf_counter() - t0) / probe_rows
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    rows = int(min(m, max(64, budget / max(per_row, 1e-9))) // 64 * 64)
+    plan_doc = _rows_plan(plan_full, rows)
+    inputs = oracle.make_inputs(kind, rows, n, k, l, seed=0, dtype=np.float32)
     for _ in range(args.warmup):
-        cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc)
+        cpu_reference_step(kind, act, rows, n, k, l, inputs, plan_doc)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc)
+        cpu_reference_step(kind, act, rows, n, k, l, inputs, plan_doc)
         times.append(time.perf_counter() - t0)
     total = float(sum(times))
-    fl = flops_of(kind, m, n, k, l)
+    fl = flops_of(kind, rows, n, k, l)
     value = fl * args.steps / total / 1e12
     cores = _blas_threads()
     return {
@@ -451,7 +508,8 @@ def run_reference(args, rank, world):
                    "path": "oracle.replay_plan: numpy restatement of fuseplan simulator.execute_plan "
                            "(the reference's CPU execution path), reference top-1 plan"},
         "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full chains m={m} (one step = one chain)"},
+                         "sample": f"{args.steps} steps, each one plan-faithful replay of a {rows}-of-{m} "
+                                   f"token-row sample of the chain (n={n} k={k} l={l})"},
         "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -493,7 +551,7 @@ def run_extra(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
