@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(256, 1) tma_mcast_kernel(const __grid_constant
       mbar_wait(full0 + 8 * stage, phase);
       if (cta_arrive)
         mbar_arrive(empty0 + 8 * stage);
+      else if (flags & 8)  // relaxed remote arrives (no release fence)
+        for (int r = 0; r < csize; ++r) mbar_arrive_remote_relaxed(mapa(empty0 + 8 * stage, r));
       else
         for (int r = 0; r < csize; ++r) mbar_arrive_remote(mapa(empty0 + 8 * stage, r));
       if (++stage == stages) { stage = 0; phase ^= 1; }
@@ -344,7 +346,7 @@ extern "C" int ff_tma_mcast_bench(const void* mat, int rows, int cols, int stage
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = (flags & 1) && csize == 1 ? 0 : 1;  // bit0: plain (non-cluster) launch
-  if (csize > 1) flags &= ~6;
+  if (csize > 1) flags &= ~6;  // bit3 (relaxed remote arrives) stays
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);

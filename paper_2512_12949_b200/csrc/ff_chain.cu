@@ -255,13 +255,13 @@ struct PairStages {
   static constexpr int value = kMax > 4 ? 4 : kMax;
 };
 
-template <bool kGated, bool kPacked>
+template <bool kGated, bool kPacked, bool kQuad>
 int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
                      cudaStream_t stream) {
   constexpr int kStages = PairStages<kGated>::value;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
   using C = ff::PairCfg<kGated, 256, kStages>;
-  auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked>;
+  auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked, kQuad>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM); });
@@ -332,7 +332,11 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   if (cfg->ring > 64) return fail(FF_ERR_UNSUPPORTED, "ring of more than 64 pairs");
-  const int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
+  int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
+  if (kQuad) {  // rings in X/Y couples, clusters of 4 co-resident
+    rings = std::min(rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring));
+    rings &= ~1;
+  }
   if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring of pairs larger than the GPU");
   ff::ChainArgs a{};
   a.M = (int)M;
@@ -376,7 +380,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   lc.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = kQuad ? 4 : 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeCooperative;
@@ -398,14 +402,32 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   return FF_OK;
 }
 
+// Quad (weight-multicast) variant when the units come in m-tile couples that
+// share their weights: an even number of m tiles, an even number of rings of
+// at most one unit each... any even ring count works (units 2j / 2j+1 pair up).
+bool quad_ok(const ffKernelConfig* cfg) {
+  if (g_dbg & 64u) return false;  // diagnostics: force the plain pair kernel
+  if (cfg->m_tiles % 2 || cfg->units % 2) return false;
+  int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
+  rings = std::min(rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring));
+  return rings >= 2;
+}
+
+template <bool kGated, bool kPacked>
+int launch_pair_q(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
+                  cudaStream_t stream) {
+  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true>(ch, cfg, t, ws, c_debug, stream)
+                      : launch_pair_impl<kGated, kPacked, false>(ch, cfg, t, ws, c_debug, stream);
+}
+
 int launch_pair_dispatch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
                          void* c_debug, cudaStream_t stream) {
-  if (ch->kind != FF_KIND_GATED) return launch_pair_impl<false, false>(ch, cfg, t, ws, c_debug, stream);
+  if (ch->kind != FF_KIND_GATED) return launch_pair_q<false, false>(ch, cfg, t, ws, c_debug, stream);
   // gate|up packed as one [2][K][N] tensor: one TMA box fetches both branches
   const bool packed = reinterpret_cast<const uint8_t*>(t->b1) ==
                       reinterpret_cast<const uint8_t*>(t->b) + (size_t)ch->k * ch->n * 2;
-  return packed ? launch_pair_impl<true, true>(ch, cfg, t, ws, c_debug, stream)
-                : launch_pair_impl<true, false>(ch, cfg, t, ws, c_debug, stream);
+  return packed ? launch_pair_q<true, true>(ch, cfg, t, ws, c_debug, stream)
+                : launch_pair_q<true, false>(ch, cfg, t, ws, c_debug, stream);
 }
 
 using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);

@@ -65,7 +65,14 @@ struct PairCfg {
   static_assert(kLB == 256 || kLB == 128, "E slice: 128 or 256 columns");
 };
 
-template <bool kGated, int kLB, int kStages, bool kPackedB>
+// kQuad: clusters of 4 = two CTA pairs at the same ring position of two rings
+// whose units differ only in the m tile (X = even ring, Y = odd ring).  Their
+// weight tiles (B / gate|up for GEMM0, D for the hops) are identical, so each
+// is TMA-multicast to both pairs by one of them (alternating per stage): three
+// TMA instructions per two stages per CTA instead of four (the TMA unit is
+// per-instruction bound: profiles/r01/mcast_relaxed.log).  Stages are freed
+// by both leaders' commits (empty-barrier count 2, commit mask 0xF).
+template <bool kGated, int kLB, int kStages, bool kPackedB, bool kQuad>
 __global__ void __launch_bounds__(256, 1)
     ff_chain_pair_kernel(const __grid_constant__ PairMaps maps, const ChainArgs args) {
   using C = PairCfg<kGated, kLB, kStages>;
@@ -77,11 +84,14 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;                  // ring members (pairs)
-  const uint32_t q = cluster_rank();     // half of the pair (0 = leader)
+  const uint32_t crank = cluster_rank();
+  const uint32_t q = crank & 1u;         // half of the pair (0 = leader)
+  const uint32_t pq = kQuad ? crank >> 1 : 0u;  // pair within the quad (0 = X, 1 = Y)
+  const uint32_t lrank = 2u * pq;        // this pair's leader rank in the cluster
   const bool leader = (q == 0);
-  const int pair = blockIdx.x / 2;
-  const int p = pair % G;                // ring position
-  const int ring = pair / G;
+  const int p = kQuad ? (int)(blockIdx.x / 4) % G : (int)(blockIdx.x / 2) % G;  // ring position
+  const int ring = kQuad ? 2 * ((int)(blockIdx.x / 4) / G) + (int)pq : (int)(blockIdx.x / 2) / G;
+  const uint16_t mcast = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));  // this CTA and its twin
   const int kblocks = args.K / C::BK;
   const int steps = args.steps;
   const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
@@ -107,12 +117,13 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t e_full = bx + 32, e_empty = bx + 40, e_load = bx + 48;
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
   const uint32_t own_slot = base + C::kOFF_OWN;
-  constexpr uint16_t kPairMask = 0x3;
+  const uint16_t kPairMask = (uint16_t)(0x3u << lrank);
+  const uint16_t kStageMask = kQuad ? (uint16_t)0xF : kPairMask;  // stage consumers: both leaders
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full_bar(s), 1);  // the leader's arrive.expect_tx covers both CTAs' bytes
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), kQuad ? 2 : 1);
     }
     mbar_init(c_full, 1);
     mbar_init(c_empty, 256);  // both CTAs' epilogues arrive on the leader's barrier
@@ -146,7 +157,8 @@ __global__ void __launch_bounds__(256, 1)
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
   };
-  const uint32_t L_c_empty = mapa(c_empty, 0), L_own_full = mapa(own_full, 0), L_e_empty = mapa(e_empty, 0);
+  const uint32_t L_c_empty = mapa(c_empty, lrank), L_own_full = mapa(own_full, lrank),
+                 L_e_empty = mapa(e_empty, lrank);
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -154,6 +166,7 @@ __global__ void __launch_bounds__(256, 1)
       unsigned long long w_empty = 0, w_flag = 0;
       const unsigned long long t_start = clock64();
       int stage = 0, phase = 0;
+      uint32_t seq = 0;  // stage-load sequence number (identical in both pairs of a quad)
       auto next = [&]() {
         if (++stage == kStages) {
           stage = 0;
@@ -176,19 +189,30 @@ __global__ void __launch_bounds__(256, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t lb = mapa(full_bar(stage), 0);
+          const uint32_t lb = mapa(full_bar(stage), lrank);
           arm();
           tma_load_3d_pair(sb, &maps.a, lb, 0, u.m0 + (int)q * C::BM, kb * (C::BK / 64));
+          const bool mine = !kQuad || ((seq++ & 1u) == pq);  // this pair issues the shared weight tile
           // L2 prefetch of the B tile `prefetch` k-blocks ahead: the weights
           // stream from HBM; the extra lead hides its latency behind 3 stages
           const int pf = args.prefetch;
-          if (pf && kb + pf < kblocks) {
+          if (pf && kb + pf < kblocks && (!kQuad || pq == 0)) {
             if (!kGated || !kPackedB)
               tma_prefetch_l2_3d(&maps.b, 0, (kb + pf) * C::BK, nblk);
             else
               tma_prefetch_l2_4d(&maps.b, 0, (kb + pf) * C::BK, nblk, 0);
           }
-          if (!kGated) {
+          if (!mine) {
+          } else if (kQuad) {
+            if (!kGated) {
+              tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast);
+            } else if (kPackedB) {
+              tma_load_4d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0, mcast);
+            } else {
+              tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast);
+              tma_load_3d_pair_mcast(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk, mcast);
+            }
+          } else if (!kGated) {
             tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
           } else if (kPackedB) {
             tma_load_4d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0);
@@ -228,17 +252,20 @@ __global__ void __launch_bounds__(256, 1)
           fence_acq_rel_gpu();
           fence_proxy_async_global();
         }
-        if (args.prefetch && h + args.prefetch < G) {  // D rows of a later hop of this step
+        if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
           const int ncol_pf = u.n0 + (t * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) tma_prefetch_l2_3d(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk);
         }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t lb = mapa(full_bar(stage), 0);
+          const uint32_t lb = mapa(full_bar(stage), lrank);
           if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
           if (from_l2) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
-          tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
+          if (!kQuad)
+            tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
+          else if ((seq++ & 1u) == pq)
+            tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, mcast);
           next();
         }
       };
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(256, 1)
               umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
             }
           }
-          umma_commit_pair(empty_bar(stage), kPairMask);
+          umma_commit_pair(empty_bar(stage), kStageMask);
           next();
         }
         if (kb1 == kblocks) umma_commit_pair(c_full, kPairMask);
@@ -325,7 +352,7 @@ __global__ void __launch_bounds__(256, 1)
                              e_started ? 1u : 0u);
             e_started = true;
           }
-          umma_commit_pair(empty_bar(stage), kPairMask);
+          umma_commit_pair(empty_bar(stage), kStageMask);
           next();
         }
         if (C::kOwnFull && h == 0) umma_commit_pair(own_free, kPairMask);

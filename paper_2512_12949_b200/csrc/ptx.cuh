@@ -84,6 +84,11 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar)
                : "memory");
 }
+// Remote arrive without release semantics (the arriving thread publishes no
+// data through it; e.g. "stage consumed" when the consumer is asynchronous).
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -224,6 +229,25 @@ __device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const void* desc,
       "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
       "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar)
+      : "memory");
+}
+// Pair loads multicast to the same offset of every CTA in `mask`; each
+// destination's complete_tx lands on its pair leader's barrier (the leader_bar
+// offset, peer bit cleared), as for the unicast pair form.
+__device__ __forceinline__ void tma_load_3d_pair_mcast(uint32_t dst, const void* desc, uint32_t leader_bar, int32_t c0,
+                                                       int32_t c1, int32_t c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_mcast(uint32_t dst, const void* desc, uint32_t leader_bar, int32_t c0,
+                                                       int32_t c1, int32_t c2, int32_t c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar), "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void tma_store_3d(const void* desc, uint32_t src, int32_t c0, int32_t c1, int32_t c2) {
