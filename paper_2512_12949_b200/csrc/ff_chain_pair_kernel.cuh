@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(256, 1)
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
-    if (issuer) bulk_wait0();  // every E store / reduction performed before exit
+    if (issuer) bulk_wait_read0();  // smem sources of the E stores read before exit (writes drain at grid end)
     if (args.prof && issuer) {
       unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
       pr[9] = clock64() - t_start;

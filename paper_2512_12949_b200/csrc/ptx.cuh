@@ -135,8 +135,12 @@ __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity)
 
 // Monotonic credit counters in shared memory (no phase aliasing, unlike an
 // mbarrier that can be completed twice before the waiter looks).
+// Remote credit / ack increment.  Relaxed: it publishes no data (the events it
+// reports -- a landed push, a consumed receive buffer -- were observed through
+// mbarriers before it is issued), and a release.cluster fence per hop costs
+// ~1 us of latency on B200 (profiles/r01/tma_variants.log).
 __device__ __forceinline__ void credit_add_remote(uint32_t cluster_addr) {
-  asm volatile("red.release.cluster.shared::cluster.add.u32 [%0], 1;" ::"r"(cluster_addr) : "memory");
+  asm volatile("red.relaxed.cluster.shared::cluster.add.u32 [%0], 1;" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
   uint32_t v;
