@@ -368,6 +368,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
                  (size_t)((M + 255) / 256) * 2 * (L / 256) * 16 <= (1u << 17);
   if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);
   a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
+  a.defer_last = (g_dbg & 128u) ? 0 : 1;
   if ((g_dbg >> 12) & 15u) a.prefetch = (int)((g_dbg >> 12) & 15u) - 1;
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);

@@ -64,6 +64,7 @@ struct ChainArgs {
   uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
   int defer;           // pair kernel: hops of step T that run after GEMM0(T+1) (< G)
+  int defer_last;      // pair kernel: run the ring's last GEMM0 before all hops of the previous step
   int prefetch;        // pair kernel: L2 prefetch distance for weight tiles (k-blocks / hops), 0 = off
   int finish_tma;      // pair kernel: split finish by bulk copies (one unit per ring, 128/S % 8 == 0)
   uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits

@@ -152,8 +152,13 @@ __global__ void __launch_bounds__(256, 1)
   // GEMM0 of step T+1 is spread over the first G - defer hops of step T; the
   // last `defer` hops run after it, while the epilogue drains C(T+1), so the
   // tensor core does not idle through the drain.
-  const int g0_slices = G - args.defer;
-  auto slot_lo = [&](int h) { return h < g0_slices ? h * kblocks / g0_slices : kblocks; };
+  // The ring's last GEMM0 runs before every hop of the previous step: nothing
+  // follows it, so all G-1 remote hops are needed to cover its drain, publish
+  // and the ring members' skew.
+  auto slot_lo = [&](int Tn, int h) {
+    const int g0_slices = (Tn == total_steps - 1 && args.defer_last) ? 1 : G - args.defer;
+    return h < g0_slices ? h * kblocks / g0_slices : kblocks;
+  };
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
   };
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(256, 1)
       if (total_steps > 0) load_gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
           load_hop(T, h);
         }
       }
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(256, 1)
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
           hop(T, h);
         }
       }
