@@ -101,6 +101,33 @@ typedef struct ffTensors {
   void* e;
 } ffTensors;
 
+/* Conv chain (ConvChainConfig, workload.py:168-199): conv(k1 x k1, stride 1,
+ * same padding) -> activation -> conv(1 x 1).  The reference lowers it to a
+ * GEMM chain over an explicit im2col matrix (conv_chain_to_gemm,
+ * workload.py:191-199: m = h*w, k = ic*k1^2, n = oc1, l = oc2); here GEMM0
+ * reads the NHWC feature map itself through an im2col TMA tensor map
+ * (implicit GEMM, no im2col matrix in HBM).  Tensors for ff_conv_chain_launch:
+ *   a = X  [batch][h][w][ic]      (NHWC)
+ *   b = W1 [k1][k1][ic][oc1]      (= [k1*k1*ic][oc1] row-major, tap-major K)
+ *   d = W2 [oc1][oc2]             (1x1 conv)
+ *   e = Y  [batch][h][w][oc2]     (NHWC)
+ * k1 > 1 needs ic % 64 == 0 and the dsm / l2 exchange (1-CTA kernels). */
+typedef struct ffConvDesc {
+  int32_t batch, h, w, ic, oc1, oc2, k1, k2;
+  int32_t activation; /* FF_ACT_* applied between the convolutions (ReLU in the reference) */
+} ffConvDesc;
+
+/* GEMM-chain view of a conv chain (m = batch*h*w unpadded). */
+int ff_conv_chain_desc(const ffConvDesc* conv, ffChainDesc* out);
+/* Physical launch configuration for a conv chain under `exchange`. */
+int ff_conv_chain_lower(const ffConvDesc* conv, int32_t num_sms, int32_t exchange, ffKernelConfig* out);
+size_t ff_conv_chain_workspace_bytes(const ffConvDesc* conv, const ffKernelConfig* cfg);
+/* Replaces execute_plan (simulator.py:177) on a conv preset's chain, reading
+ * X instead of its im2col matrix.  `cfg` from ff_conv_chain_lower or from
+ * ff_plan_lower_ex on ff_conv_chain_desc. */
+int ff_conv_chain_launch(const ffConvDesc* conv, const ffKernelConfig* cfg, const ffTensors* t, void* workspace,
+                         size_t ws_bytes, void* stream);
+
 /* Lower a reference plan to a physical launch (no GPU work).  The plan's
  * cls_shuffle ring becomes one thread-block cluster exchanging C over DSM. */
 int ff_plan_lower(const ffChainDesc* chain, const ffPlanDesc* plan, int32_t num_sms, ffKernelConfig* out);

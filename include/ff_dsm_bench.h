@@ -31,6 +31,15 @@ int ff_tma_stream_bench(const void* mat, int rows, int cols, int stages, int ite
 int ff_tma_mcast_bench(const void* mat, int rows, int cols, int stages, int iters, int box_rows, int box_blocks,
                        int csize, int ctas, int stage_bytes, int flags, float* ms_out);
 
+/* Diagnostics: one 1-thread kernel writing %globaltimer (ns) to *dst on `stream`;
+ * brackets a launch on the GPU's own clock (launch latency / drain tail). */
+int ff_stamp_globaltimer(void* dst, void* stream);
+
+/* Diagnostics: an empty kernel with a chain kernel's launch shape (`ctas` x 256
+ * threads, `smem_bytes` dynamic smem, clusters of `cluster`, optional 512-column
+ * TMEM alloc/dealloc); CTA i writes entry/exit %globaltimer to stamps[2i], [2i+1]. */
+int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tmem, void* stream);
+
 const char* ff_dsm_last_error(void);
 
 #ifdef __cplusplus

@@ -184,3 +184,28 @@ def replay_plan(kind: str, activation: str, dims: tuple, plan: dict, inputs: dic
                     last_g1 = key
                     fire(ready["inc"], leaf)
     return e_out
+
+
+def im2col_nhwc(x: np.ndarray, k1: int) -> np.ndarray:
+    """The reference's conv lowering made explicit (conv_chain_to_gemm,
+    workload.py:191-199: m = h*w, k = ic*k1^2): x [batch, h, w, ic] NHWC ->
+    A [batch*h*w, k1*k1*ic] with K ordered (tap r, tap s, channel), stride 1,
+    same padding (zeros outside the image)."""
+    b, h, w, c = x.shape
+    pad = k1 // 2
+    xp = np.zeros((b, h + 2 * pad, w + 2 * pad, c), dtype=x.dtype)
+    xp[:, pad:pad + h, pad:pad + w, :] = x
+    cols = [xp[:, r:r + h, s:s + w, :] for r in range(k1) for s in range(k1)]
+    return np.concatenate(cols, axis=-1).reshape(b * h * w, k1 * k1 * c)
+
+
+def conv_chain(x: np.ndarray, w1: np.ndarray, w2: np.ndarray, activation: str = "relu",
+               bf16_intermediate: bool = False) -> np.ndarray:
+    """conv(k1 x k1, same) -> act -> conv(1x1) as the GEMM chain the reference
+    executes on a conv preset (dense_chain over the im2col matrix).
+    x [b, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2] -> y [b, h, w, oc2]."""
+    b, h, w, _ = x.shape
+    k1 = w1.shape[0]
+    inputs = {"A": im2col_nhwc(x, k1), "B": w1.reshape(-1, w1.shape[-1]), "D": w2}
+    y = dense_chain("standard_ffn", activation, inputs, bf16_intermediate=bf16_intermediate)
+    return y.reshape(b, h, w, w2.shape[1])

@@ -42,6 +42,10 @@ EXPORTS = (
     "ff_set_profile_buffer",
     "ff_last_error",
     "ff_version",
+    "ff_conv_chain_desc",
+    "ff_conv_chain_lower",
+    "ff_conv_chain_workspace_bytes",
+    "ff_conv_chain_launch",
 )
 
 
@@ -99,6 +103,12 @@ class KernelConfig(ctypes.Structure):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
+class ConvDesc(ctypes.Structure):
+    """ffConvDesc: ConvChainConfig (workload.py:168-184) + batch and activation."""
+
+    _fields_ = [(name, ctypes.c_int32) for name in ("batch", "h", "w", "ic", "oc1", "oc2", "k1", "k2", "activation")]
+
+
 class Tensors(ctypes.Structure):
     _fields_ = [
         ("a", ctypes.c_void_p),
@@ -139,6 +149,12 @@ def load(path: str = LIB_PATH):
                                               ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
         lib.ff_chain_kernel_count.argtypes = [P(ChainDesc), P(KernelConfig)]
         lib.ff_set_profile_buffer.argtypes = [ctypes.c_void_p]
+        lib.ff_conv_chain_desc.argtypes = [P(ConvDesc), P(ChainDesc)]
+        lib.ff_conv_chain_lower.argtypes = [P(ConvDesc), ctypes.c_int32, ctypes.c_int32, P(KernelConfig)]
+        lib.ff_conv_chain_workspace_bytes.argtypes = [P(ConvDesc), P(KernelConfig)]
+        lib.ff_conv_chain_workspace_bytes.restype = ctypes.c_size_t
+        lib.ff_conv_chain_launch.argtypes = [P(ConvDesc), P(KernelConfig), P(Tensors), ctypes.c_void_p,
+                                             ctypes.c_size_t, ctypes.c_void_p]
         lib.ff_last_error.restype = ctypes.c_char_p
         lib.ff_version.restype = ctypes.c_char_p
         _lib = lib

@@ -64,6 +64,49 @@ __global__ void __launch_bounds__(128, 1) dsm_push_kernel(int chunk, int depth, 
   cluster_sync();
 }
 
+__global__ void stamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+// Launch-overhead probe: an otherwise empty kernel with the launch shape of
+// the chain kernels (dynamic smem, cluster, TMEM alloc); stamps entry/exit.
+__global__ void __launch_bounds__(256, 1) launch_probe_kernel(unsigned long long* stamps, int tmem) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  using namespace ff;
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[2 * blockIdx.x] = t;
+  }
+  if (tmem && threadIdx.x / 32 == 1) tmem_alloc<512>(smem_u32(smem));
+  __syncthreads();
+  if (tmem && threadIdx.x / 32 == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(*reinterpret_cast<volatile uint32_t*>(smem));
+  }
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[2 * blockIdx.x + 1] = t;
+  }
+}
+
+struct BigParams {
+  unsigned long long pad[176];  // 1408 B, the size of PairMaps
+};
+__global__ void __launch_bounds__(256, 1) launch_probe_big_kernel(const __grid_constant__ BigParams bp,
+                                                                  unsigned long long* stamps) {
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[2 * blockIdx.x] = t + (bp.pad[threadIdx.x + 100] & 1ull);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[2 * blockIdx.x + 1] = t;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -128,6 +171,50 @@ int ff_max_active_clusters(int cluster, int smem_bytes, int* out) {
   cudaFuncSetAttribute(dsm_push_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   cudaFuncSetAttribute(dsm_push_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaError_t e = cudaOccupancyMaxActiveClusters(out, dsm_push_kernel, &lc);
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tmem, void* stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(launch_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+    cudaFuncSetAttribute(launch_probe_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(ctas, 1, 1);
+  lc.blockDim = dim3(256, 1, 1);
+  lc.dynamicSmemBytes = smem_bytes;
+  lc.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute a[1];
+  a[0].id = cudaLaunchAttributeClusterDimension;
+  a[0].val.clusterDim.x = cluster;
+  a[0].val.clusterDim.y = 1;
+  a[0].val.clusterDim.z = 1;
+  lc.attrs = a;
+  lc.numAttrs = cluster > 1 ? 1 : 0;
+  cudaError_t e;
+  if (tmem == 2) {
+    BigParams bp = {};
+    lc.dynamicSmemBytes = 0;
+    e = cudaLaunchKernelEx(&lc, launch_probe_big_kernel, bp, reinterpret_cast<unsigned long long*>(stamps));
+  } else {
+    e = cudaLaunchKernelEx(&lc, launch_probe_kernel, reinterpret_cast<unsigned long long*>(stamps), tmem);
+  }
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+int ff_stamp_globaltimer(void* dst, void* stream) {
+  stamp_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<unsigned long long*>(dst));
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_err = cudaGetErrorString(e);
     return 4;

@@ -44,6 +44,53 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  });
+  return fn;
+}
+
+// NHWC bf16 feature map [n][h][w][c] -> im2col map for a k1 x k1, stride-1,
+// same-padding convolution: boxes of 128 output pixels x 64 channels (one
+// 128-byte SW128 row per pixel, the K-major UMMA A layout).  Bounding box
+// corners -pad / pad-(k1-1) make the traversal enumerate exactly the h x w
+// output positions; the tap offsets (s, r) then address the input pixel and
+// out-of-image taps read zeros.
+bool make_map_im2col(CUtensorMap* map, const void* ptr, const ffConvDesc* cv) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  if (!fn) return false;
+  const int pad = cv->k1 / 2;
+  cuuint64_t dims[4] = {(cuuint64_t)cv->ic, (cuuint64_t)cv->w, (cuuint64_t)cv->h, (cuuint64_t)cv->batch};
+  cuuint64_t strides[3] = {(cuuint64_t)cv->ic * 2, (cuuint64_t)cv->w * cv->ic * 2,
+                           (cuuint64_t)cv->h * cv->w * cv->ic * 2};
+  int lower[2] = {-pad, -pad};
+  int upper[2] = {pad - (cv->k1 - 1), pad - (cv->k1 - 1)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, lower, upper, 64,
+                  128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  // Same descriptor fix-up as CUTLASS's make_im2col_tma_copy for drivers
+  // <= 13.1 on tensors below 128 KB (cute/atom/copy_traits_sm90_im2col.hpp).
+  int drv = 0;
+  if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 &&
+      (uint64_t)cv->batch * cv->h * cv->w * cv->ic * 2 < 131072)
+    reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return true;
+}
+
 // Row-major bf16 matrix [rows][cols] -> 2-D map with a (box_cols x box_rows) box, 128B swizzle.
 bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
               uint32_t box_rows) {
@@ -158,7 +205,7 @@ uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
 
 template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
-                void* c_debug, cudaStream_t stream) {
+                void* c_debug, cudaStream_t stream, const ffConvDesc* conv) {
   constexpr int kStages = StagesFor<kGated, kNB, kLB, kMode>::value;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
   using C = ff::ChainCfg<kGated, kNB, kLB, kStages, kMode>;
@@ -178,7 +225,8 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   const WsLayout wl = ws_layout(ch, cfg);
   uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
   CUtensorMap mA, mB0, mB1, mD, mC;
-  bool ok = make_map(&mA, t->a, M, K, 64, 128);
+  const bool implicit = conv != nullptr && conv->k1 > 1;
+  bool ok = implicit ? make_map_im2col(&mA, t->a, conv) : make_map(&mA, t->a, M, K, 64, 128);
   ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
   ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
   ok = ok && make_map(&mD, t->d, N, L, 64, 64);
@@ -236,6 +284,12 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
+  if (implicit) {
+    a.conv_k1 = conv->k1;
+    a.conv_H = conv->h;
+    a.conv_W = conv->w;
+    a.conv_cblk = conv->ic / 64;
+  }
 
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
@@ -257,7 +311,7 @@ struct PairStages {
 
 template <bool kGated, bool kPacked, bool kQuad>
 int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
-                     cudaStream_t stream) {
+                     cudaStream_t stream, const ffConvDesc*) {
   constexpr int kStages = PairStages<kGated>::value;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
   using C = ff::PairCfg<kGated, 256, kStages>;
@@ -416,22 +470,24 @@ bool quad_ok(const ffKernelConfig* cfg) {
 
 template <bool kGated, bool kPacked>
 int launch_pair_q(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
-                  cudaStream_t stream) {
-  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true>(ch, cfg, t, ws, c_debug, stream)
-                      : launch_pair_impl<kGated, kPacked, false>(ch, cfg, t, ws, c_debug, stream);
+                  cudaStream_t stream, const ffConvDesc* conv) {
+  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true>(ch, cfg, t, ws, c_debug, stream, conv)
+                      : launch_pair_impl<kGated, kPacked, false>(ch, cfg, t, ws, c_debug, stream, conv);
 }
 
 int launch_pair_dispatch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
-                         void* c_debug, cudaStream_t stream) {
-  if (ch->kind != FF_KIND_GATED) return launch_pair_q<false, false>(ch, cfg, t, ws, c_debug, stream);
+                         void* c_debug, cudaStream_t stream, const ffConvDesc* conv) {
+  if (conv != nullptr && conv->k1 > 1) return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv needs the 1-CTA kernel");
+  if (ch->kind != FF_KIND_GATED) return launch_pair_q<false, false>(ch, cfg, t, ws, c_debug, stream, conv);
   // gate|up packed as one [2][K][N] tensor: one TMA box fetches both branches
   const bool packed = reinterpret_cast<const uint8_t*>(t->b1) ==
                       reinterpret_cast<const uint8_t*>(t->b) + (size_t)ch->k * ch->n * 2;
-  return packed ? launch_pair_q<true, true>(ch, cfg, t, ws, c_debug, stream)
-                : launch_pair_q<true, false>(ch, cfg, t, ws, c_debug, stream);
+  return packed ? launch_pair_q<true, true>(ch, cfg, t, ws, c_debug, stream, conv)
+                : launch_pair_q<true, false>(ch, cfg, t, ws, c_debug, stream, conv);
 }
 
-using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t);
+using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t,
+                         const ffConvDesc*);
 
 LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
   if (mode == FF_XCHG_L2_PAIR) {
@@ -636,7 +692,7 @@ int ff_chain_kernel_count(const ffChainDesc* ch, const ffKernelConfig* cfg) {
 }
 
 static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, const ffTensors* t, void* ws,
-                         size_t ws_bytes, void* c_debug, void* stream) {
+                         size_t ws_bytes, void* c_debug, void* stream, const ffConvDesc* conv = nullptr) {
   int rc = validate_chain(ch);
   if (rc) return rc;
   if (!cfg_in || !t || !t->a || !t->b || !t->d || !t->e) return fail(FF_ERR_ARG, "null tensor pointer");
@@ -658,7 +714,7 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
     return fail(FF_ERR_UNSUPPORTED, "too many E tiles for the split arrival counters");
   if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(FF_ERR_ARG, "workspace must be 256-byte aligned");
   LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb, cfg.exchange);
-  return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream));
+  return fn(ch, &cfg, t, ws, c_debug, reinterpret_cast<cudaStream_t>(stream), conv);
 }
 
 int ff_chain_launch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
@@ -669,6 +725,54 @@ int ff_chain_launch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTe
 int ff_chain_launch_debug(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
                           size_t ws_bytes, void* c_out, void* stream) {
   return launch_common(ch, cfg, t, ws, ws_bytes, c_out, stream);
+}
+
+// ---- conv chain (workload.py:168-199) as an implicit GEMM ----
+int ff_conv_chain_desc(const ffConvDesc* cv, ffChainDesc* out) {
+  if (!cv || !out) return fail(FF_ERR_ARG, "null conv descriptor or output");
+  if (cv->batch < 1 || cv->h < 1 || cv->w < 1 || cv->ic < 1 || cv->oc1 < 1 || cv->oc2 < 1 || cv->k1 < 1 || cv->k2 < 1)
+    return fail(FF_ERR_ARG, "conv extents must be positive");
+  if (cv->k2 != 1) return fail(FF_ERR_UNSUPPORTED, "only a pointwise (1x1) second convolution is supported");
+  if (cv->k1 % 2 == 0) return fail(FF_ERR_UNSUPPORTED, "same padding needs an odd filter size");
+  if (cv->k1 > 1 && cv->ic % 64)
+    return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv needs input channels in multiples of 64");
+  if (cv->k1 > 1 && (cv->k1 / 2 > 127 || cv->h > 65535 || cv->w > 65535))
+    return fail(FF_ERR_UNSUPPORTED, "filter / feature map outside the im2col TMA ranges");
+  ffChainDesc ch = {};
+  ch.kind = FF_KIND_STANDARD;
+  ch.activation = cv->activation;
+  ch.m = (int64_t)cv->batch * cv->h * cv->w;
+  ch.n = cv->oc1;
+  ch.k = (int64_t)cv->k1 * cv->k1 * cv->ic;
+  ch.l = cv->oc2;
+  ch.element_size = 2;
+  *out = ch;
+  return validate_chain(&ch);
+}
+
+int ff_conv_chain_lower(const ffConvDesc* cv, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {
+  ffChainDesc ch;
+  int rc = ff_conv_chain_desc(cv, &ch);
+  if (rc) return rc;
+  if (cv->k1 > 1 && exchange == FF_XCHG_L2_PAIR)
+    return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv runs on the 1-CTA kernels (dsm / l2 exchange)");
+  return ff_auto_config_ex(&ch, num_sms, exchange, out);
+}
+
+size_t ff_conv_chain_workspace_bytes(const ffConvDesc* cv, const ffKernelConfig* cfg) {
+  ffChainDesc ch;
+  if (ff_conv_chain_desc(cv, &ch)) return 0;
+  return ff_chain_workspace_bytes(&ch, cfg);
+}
+
+int ff_conv_chain_launch(const ffConvDesc* cv, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
+                         size_t ws_bytes, void* stream) {
+  ffChainDesc ch;
+  int rc = ff_conv_chain_desc(cv, &ch);
+  if (rc) return rc;
+  if (cfg && cv->k1 > 1 && cfg->exchange == FF_XCHG_L2_PAIR)
+    return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv runs on the 1-CTA kernels (dsm / l2 exchange)");
+  return launch_common(&ch, cfg, t, ws, ws_bytes, nullptr, stream, cv);
 }
 
 int ff_chain_run_plan(const ffChainDesc* ch, const ffPlanDesc* plan, const ffTensors* t, void* ws,

@@ -67,6 +67,11 @@ struct ChainArgs {
   int defer_last;      // pair kernel: run the ring's last GEMM0 before all hops of the previous step
   int prefetch;        // pair kernel: L2 prefetch distance for weight tiles (k-blocks / hops), 0 = off
   int finish_tma;      // pair kernel: split finish by bulk copies (one unit per ring, 128/S % 8 == 0)
+  // conv chain as implicit GEMM (conv_k1 > 1): A is an NHWC feature map read
+  // through an im2col tensor map; GEMM0 k-block kb = (filter tap, 64-channel block)
+  int conv_k1;         // filter size of the first convolution (0: plain A[M][K])
+  int conv_H, conv_W;  // feature map height / width (M = batch * H * W output pixels)
+  int conv_cblk;       // input channels / 64
   uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits
   unsigned long long* prof;  // optional diagnostics: per CTA [FF_PROF_STRIDE] = 16 wait-cycle counters + 16 globaltimer stamps
 };
@@ -337,7 +342,16 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);
-          tma_load_2d(sb, &tmA, full_bar(stage), kb * C::BK, u.m0);
+          if (args.conv_k1 > 1) {
+            // implicit GEMM: 128 output pixels x 64 channels of filter tap (r, s)
+            const int cb = kb % args.conv_cblk, tap = kb / args.conv_cblk;
+            const int pad = args.conv_k1 / 2, hw = args.conv_H * args.conv_W;
+            const int img = u.m0 / hw, rem = u.m0 % hw;
+            tma_load_im2col_4d(sb, &tmA, full_bar(stage), cb * 64, rem % args.conv_W - pad, rem / args.conv_W - pad,
+                               img, (uint16_t)(tap % args.conv_k1), (uint16_t)(tap / args.conv_k1));
+          } else {
+            tma_load_2d(sb, &tmA, full_bar(stage), kb * C::BK, u.m0);
+          }
           if (kGated) {
             tma_load_2d(sb + C::kA_BYTES, &tmB0, full_bar(stage), n0, kb * C::BK);
             tma_load_2d(sb + C::kA_BYTES + C::BK * kNB * 2, &tmB1, full_bar(stage), n0, kb * C::BK);

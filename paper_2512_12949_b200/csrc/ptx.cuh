@@ -211,6 +211,19 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* desc, uint
       "l"(desc), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// im2col mode over an NHWC tensor map (cuTensorMapEncodeIm2col): a box of
+// pixelsPerColumn consecutive output pixels x channelsPerPixel channels,
+// starting at bounding-box position (c, w, h, n), each pixel displaced by the
+// filter tap (off_w, off_h); out-of-image taps are zero-filled (padding).
+__device__ __forceinline__ void tma_load_im2col_4d(uint32_t dst, const void* desc, uint32_t bar, int32_t c,
+                                                   int32_t w, int32_t h, int32_t n, uint16_t off_w,
+                                                   uint16_t off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(dst),
+      "l"(desc), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(off_w), "h"(off_h)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* desc, uint32_t bar, int32_t c0, int32_t c1,
                                             int32_t c2) {
   asm volatile(

@@ -14,7 +14,7 @@ from typing import Optional
 
 from . import _native as nat
 from .plan import FusionPlan
-from .workload import DIMS, GATED_FFN, ChainGraph
+from .workload import DIMS, GATED_FFN, ChainGraph, ConvChainConfig
 
 _workspaces: dict = {}
 
@@ -199,3 +199,63 @@ def profile_configs(graph: ChainGraph, cfgs, tensors: dict, iters: int = 10, war
         stop.synchronize()
         out.append((start.elapsed_time(stop) / iters, cfg))
     return out
+
+
+# ----------------------------------------------------------------------------- conv chains
+
+
+def conv_desc(cfg: ConvChainConfig, batch: int = 1, activation: str = "relu") -> nat.ConvDesc:
+    return nat.ConvDesc(batch, cfg.h, cfg.w, cfg.ic, cfg.oc1, cfg.oc2, cfg.k1, cfg.k2, nat.ACT[activation])
+
+
+def lower_conv(cfg: ConvChainConfig, batch: int = 1, exchange: str = "auto", activation: str = "relu",
+               num_sms: Optional[int] = None) -> nat.KernelConfig:
+    """Physical launch for a conv chain (ConvChainConfig, workload.py:168-184).
+    k1 > 1 runs as an implicit GEMM on the 1-CTA kernels ("dsm" / "l2")."""
+    lib = nat.load()
+    cd = conv_desc(cfg, batch, activation)
+    order = {"auto": ("pair", "l2", "dsm")}.get(exchange, (exchange,))
+    last = None
+    for x in order:
+        out = nat.KernelConfig()
+        try:
+            nat.check(lib.ff_conv_chain_lower(ctypes.byref(cd), num_sms or 148, EXCHANGES[x], ctypes.byref(out)))
+            return out
+        except nat.UnsupportedPlan as exc:
+            last = exc
+    raise last
+
+
+def launch_conv(cfg: ConvChainConfig, kcfg: nat.KernelConfig, x, w1, w2, out=None, stream=None,
+                activation: str = "relu"):
+    """conv(k1 x k1, same padding) -> act -> conv(1 x 1) on NHWC bf16 tensors:
+    x [batch, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2]; returns
+    y [batch, h, w, oc2].  GEMM0 reads x through an im2col tensor map."""
+    import torch
+
+    lib = nat.load()
+    if not torch.cuda.is_available():
+        raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
+    batch = x.shape[0]
+    shapes = {"x": (batch, cfg.h, cfg.w, cfg.ic), "w1": (cfg.k1, cfg.k1, cfg.ic, cfg.oc1), "w2": (cfg.oc1, cfg.oc2)}
+    for name, t in (("x", x), ("w1", w1), ("w2", w2)):
+        if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
+    if out is None:
+        out = torch.empty((batch, cfg.h, cfg.w, cfg.oc2), dtype=torch.bfloat16, device=x.device)
+    cd = conv_desc(cfg, batch, activation)
+    ws_bytes = lib.ff_conv_chain_workspace_bytes(ctypes.byref(cd), ctypes.byref(kcfg))
+    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    ws = _workspace(ws_bytes, x.device, s)
+    tp = nat.Tensors(x.data_ptr(), w1.data_ptr(), None, w2.data_ptr(), out.data_ptr())
+    nat.check(lib.ff_conv_chain_launch(ctypes.byref(cd), ctypes.byref(kcfg), ctypes.byref(tp),
+                                       ws.data_ptr() if ws is not None else None, ws_bytes, s.cuda_stream))
+    return out
+
+
+def run_conv(cfg: ConvChainConfig, x, w1, w2, out=None, stream=None, exchange: str = "auto",
+             activation: str = "relu"):
+    """Execute a conv chain on the current GPU (the reference's conv presets
+    C1-C8, workload.py:207-240, without materialising the im2col matrix)."""
+    kcfg = lower_conv(cfg, x.shape[0], exchange, activation, _num_sms())
+    return launch_conv(cfg, kcfg, x, w1, w2, out=out, stream=stream, activation=activation)
