@@ -108,7 +108,8 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, u
 
 // Generic N-D map (dims innermost first; strides in bytes for dims 1..rank-1).
 bool make_map_nd(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
-                 const uint64_t* strides, const uint32_t* box) {
+                 const uint64_t* strides, const uint32_t* box,
+                 CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t d[5], st[4];
@@ -120,7 +121,7 @@ bool make_map_nd(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void*
     if (i + 1 < rank) st[i] = strides[i];
   }
   return fn(map, dt, rank, const_cast<void*>(ptr), d, st, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+            swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
@@ -194,7 +195,8 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
   if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
   w.s_off = off;
-  if (pair && c->n_splits > 1) off = align256(off + (size_t)c->n_splits * ch->m * ch->l * sizeof(float));
+  if (pair && c->n_splits > 1)
+    off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * 256 * ch->l * sizeof(float));
   w.total = off;
   return w;
 }
@@ -377,11 +379,15 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const uint64_t dw[3] = {32, M, L / 32}, sw[2] = {L * 4, 128};
     const uint32_t bw[3] = {32, 128, 256 / 32};
     ok = ok && make_map_nd(&maps.w3, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, wp, dw, sw, bw);
+    // split-N exchange regions [E tile][split][16-byte chunk][128 rows] x 16 B as a 3D
+    // {8 rows x 4 floats, 16 row groups, chunk}: box {32, 128/S/8, 64} = one split's
+    // rows of a slice, 128-byte inner rows (lands as [chunk][row][16 B] in smem)
     const uint64_t S = (uint64_t)std::max(1, cfg->n_splits);
     const void* sp = cfg->n_splits > 1 ? (const void*)(wsb + wl.s_off) : t->e;
-    const uint64_t ds[4] = {32, M, S, L / 32}, ss[3] = {L * 4, M * L * 4, 128};
-    const uint32_t bs[4] = {32, rs, 1, 256 / 32};
-    ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, sp, ds, ss, bs);
+    const uint64_t tiles = (uint64_t)cfg->m_tiles * 2 * (L / 256);
+    const uint64_t ds[3] = {32, 16, tiles * S * 64}, ss[2] = {128, 2048};
+    const uint32_t bs[3] = {32, rs / 8, 64};
+    ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sp, ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
@@ -410,6 +416,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
   a.tile_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off);
+  a.slab = reinterpret_cast<float*>(wsb + wl.s_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
@@ -417,7 +424,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
   a.defer = cfg->ring - 1 - cfg->ring / 4;  // measured: 3/4 of the hops (profiles/r01/cfgs_defer.log)
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
-  a.finish_tma = cfg->n_splits > 1 && cfg->n_splits <= 16 && cfg->units <= rings && 128 % cfg->n_splits == 0 &&
+  a.finish_tma = cfg->n_splits > 1 && cfg->n_splits <= 8 && cfg->units <= rings && 128 % cfg->n_splits == 0 &&
                  (128 / cfg->n_splits) % 8 == 0 &&
                  (size_t)((M + 255) / 256) * 2 * (L / 256) * 16 <= (1u << 17);
   if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);

@@ -61,6 +61,7 @@ struct ChainArgs {
   __nv_bfloat16* E;    // output (S == 1)
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
+  float* slab;         // pair kernel: split-N exchange regions [E tile][split][16-B chunk][128 rows]
   uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
   int defer;           // pair kernel: hops of step T that run after GEMM0(T+1) (< G)

@@ -37,7 +37,7 @@ struct PairMaps {
   CUtensorMap e3;   // E bf16 3D {64, M, L/64}, box {64, 128, kLB/64}
   CUtensorMap w3;   // fp32 workspace 3D {32, M, L/32}, box {32, 128, kLB/32}
   CUtensorMap er;   // E bf16 3D, box {64, 128/S, kLB/64}: one row slice of a tile
-  CUtensorMap slab; // fp32 split partials 4D {32, M, S, L/32}, box {32, 128/S, 1, kLB/32}
+  CUtensorMap slab; // split-N exchange regions 3D {32, 16, tiles*S*64} fp32, box {32, 128/S/8, 64} (no swizzle)
 };
 
 template <bool kGated, int kLB, int kStages>
@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(256, 1)
   };
   const uint32_t L_c_empty = mapa(c_empty, lrank), L_own_full = mapa(own_full, lrank),
                  L_e_empty = mapa(e_empty, lrank);
+  // Split-N reduce-scatter tail (one unit per ring, S > 1): all eight warps
+  // drain the ring's last E partial after the role loops (see below).
+  const bool scatter_all = args.S > 1 && args.finish_tma && total_steps > 0;
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -390,92 +393,6 @@ __global__ void __launch_bounds__(256, 1)
     const unsigned long long t_start = clock64();
     // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
     auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
-    // Split-N reduce-scatter for a ring's final unit when every unit is some
-    // ring's final one (no wait can then block another unit).  The fp32 E
-    // partial is staged slice-major -- [S slices][kLB/32 col groups][R rows][128 B],
-    // R = 128/S -- so split s keeps slice s in shared memory, TMA-stores every
-    // other slice j into its slab (j's row slice of split s's partial), flags it,
-    // then loads the S-1 partner slices of slice s, sums the S partials in split
-    // order (deterministic) and TMA-stores bf16 E rows [s*R, s*R+R).  Plain
-    // bulk stores and loads only: no atomics, nothing to re-zero.
-    auto slab_flag = [&](int tile, int s_) { return args.flags + (1u << 17) + tile * 16 + s_; };
-    auto split_reduce_scatter = [&](const Unit& u, int row0) {
-      const int S = args.S, R = C::BM / S, sp = u.split;
-      const int tile = (row0 / C::BM) * (args.L / kLB) + u.l0 / kLB;
-      if (issuer) {
-        for (int j = 0; j < S; ++j)
-          if (j != sp) tma_store_4d(&maps.slab, base + j * (R * 1024), 0, row0 + j * R, sp, u.l0 / 32);
-        bulk_commit();
-        bulk_wait0();  // slices written to the slab
-        fence_proxy_async_global();
-        st_release_gpu_u32(slab_flag(tile, sp), args.epoch);
-        if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
-        // partners' slices of this row slice
-        uint32_t polls = 0;
-        for (int j = 0; j < S; ++j) {
-          if (j == sp) continue;
-          while ((int)(ld_relaxed_gpu_u32(slab_flag(tile, j)) - args.epoch) < 0)
-            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
-        }
-        fence_acq_rel_gpu();
-        fence_proxy_async_global();
-        if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 27] = globaltimer_ns();
-        mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kLB * 4));
-        for (int j = 0; j < S; ++j)
-          if (j != sp) tma_load_4d(base + j * (R * 1024), &maps.slab, e_load, 0, row0 + sp * R, j, u.l0 / 32);
-      }
-      mbar_wait(e_load, 0);
-      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 28] = globaltimer_ns();
-      // sum in split order, cast, stage bf16 [kLB/64][R][128 B] after the fp32 area
-      const uint32_t ebuf_off = C::BM * kLB * 4;
-      const uint8_t* const src = smem_gen;
-      const int n_items = (args.dbg & 32u) ? 0 : R * (kLB / 4);  // diagnostics: skip the sum
-      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 29] = globaltimer_ns();
-      // four independent items per thread in flight (loads first, then adds)
-      __syncwarp();
-#pragma unroll 1
-      for (int it0 = row; it0 < n_items; it0 += 512) {
-        uint32_t off[4];
-        float4 acc[4];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int it = it0 + 128 * q4;
-          const int r = it / (kLB / 4), c16 = it % (kLB / 4);
-          off[q4] = (c16 / 8) * (R * 128) + r * 128 + (((c16 % 8) ^ (r & 7)) << 4);
-          acc[q4] = *reinterpret_cast<const float4*>(src + off[q4]);
-        }
-#pragma unroll 1
-        for (int j = 1; j < S; ++j) {
-          float4 f[4];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) f[q4] = *reinterpret_cast<const float4*>(src + j * (R * 1024) + off[q4]);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            acc[q4].x += f[q4].x;
-            acc[q4].y += f[q4].y;
-            acc[q4].z += f[q4].z;
-            acc[q4].w += f[q4].w;
-          }
-        }
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int it = it0 + 128 * q4;
-          const int r = it / (kLB / 4), c16 = it % (kLB / 4);
-          const int ch = (c16 % 16) / 2;
-          *reinterpret_cast<uint2*>(smem_gen + ebuf_off + (c16 / 16) * (R * 128) + r * 128 + ((ch ^ (r & 7)) << 4) +
-                                    (c16 & 1) * 8) =
-              make_uint2(pack_bf16x2(acc[q4].x, acc[q4].y), pack_bf16x2(acc[q4].z, acc[q4].w));
-        }
-      }
-      const uint32_t ebuf = base + ebuf_off;
-      if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 22] = globaltimer_ns();
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (issuer) {
-        tma_store_3d(&maps.er, ebuf, 0, row0 + sp * R, u.l0 / 64);
-        bulk_commit();
-      }
-    };
     for (int T = 0; T < total_steps; ++T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
@@ -546,7 +463,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (args.prof) t_store += clock64() - t_s0;
       if (issuer && T < 2) FF_STAMP(20 + 3 * T);
-      if (t == steps - 1) {
+      if (t == steps - 1 && !(scatter_all && T == total_steps - 1)) {
         // E slice: TMEM -> registers -> SW128 smem tiles in the own slot -> TMA
         // store (bf16) or TMA reduce-add into the fp32 workspace (N splits).
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
@@ -568,26 +485,7 @@ __global__ void __launch_bounds__(256, 1)
         if (final_unit) {
           // whole E tile staged at once: [kLB/cols_per_tile][128 rows][128 B] SW128 tiles, one TMA instruction
 #pragma unroll 1
-          const bool scatter = !bf16_out && args.finish_tma;
-          if (scatter) {
-            // slice-major staging: row -> (slice, row in slice); two TMEM loads per wait
-            const int R = C::BM / args.S;
-            const int rr = row % R;
-            float4* const rbase = reinterpret_cast<float4*>(smem_gen + (row / R) * (R * 1024) + rr * 128);
-#pragma unroll 1
-            for (int c0 = 0; c0 < kLB; c0 += 64) {
-              float v[32], w[32];
-              tmem_ld32x2(lane_base + C::kTMEM_E + c0, lane_base + C::kTMEM_E + c0 + 32, v, w);
-              float4* const d0 = rbase + (c0 / 32) * (R * 8);
-              float4* const d1 = d0 + R * 8;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                d0[j ^ (rr & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                d1[j ^ (rr & 7)] = make_float4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
-              }
-            }
-          }
-          for (int c0 = 0; c0 < (scatter ? 0 : kLB); c0 += 32) {
+          for (int c0 = 0; c0 < kLB; c0 += 32) {
             float v[32];
             tmem_ld32(lane_base + C::kTMEM_E + c0, v);
             const uint32_t tile = base + (c0 / cols_per_tile) * 16384;
@@ -610,11 +508,7 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive_remote(L_e_empty);
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
-          if (scatter) {
-            if (issuer) FF_STAMP(24);
-            split_reduce_scatter(u, erow);
-            if (issuer) FF_STAMP(26);
-          } else if (issuer) {
+          if (issuer) {
             if (bf16_out)
               tma_store_3d(&maps.e3, base, 0, erow, u.l0 / 64);
             else if (args.dbg & 8u)  // diagnostics: plain store instead of reduce-add (wrong sums)
@@ -626,7 +520,7 @@ __global__ void __launch_bounds__(256, 1)
             bulk_commit();
             FF_STAMP(24);
           }
-          if (!bf16_out && !scatter) {
+          if (!bf16_out) {
             split_finish<kLB>(args, tile_counter, tmem_slot + 8, issuer, true, erow, row, u.l0, 1, false);
             if (issuer) FF_STAMP(26);
           }
@@ -689,6 +583,133 @@ __global__ void __launch_bounds__(256, 1)
       pr[12] = t_drain;
       pr[13] = t_store;
       pr[14] = t_e;
+    }
+  }
+
+  if (scatter_all) {
+    // ===================== split-N reduce-scatter (all 8 warps) =====================
+    // The ring's final E partial (fp32, this CTA's 128 rows x kLB columns) never
+    // touches shared memory: row slice j (R = 128/S rows) belongs to split j.
+    // Threads holding rows of another split's slice write them straight from
+    // TMEM registers into this split's exchange region, laid out
+    // [16-byte column chunk][row] so that a warp's 32 rows form one contiguous
+    // 512-byte store (and later load); then the CTA flags the region.  Threads
+    // holding rows of the own slice wait for the partners' flags, sum the S
+    // partials in split order (deterministic, own partial from TMEM), cast to
+    // bf16 and stage the rows for one TMA store of E.  Warp w reads TMEM lane
+    // quarter w%4; warps 0-3 take the upper half of the columns.
+    const Unit u = unit_of(my_units - 1);
+    const int S = args.S, R = C::BM / S, sp = u.split;
+    const int erow = u.m0 + (int)q * C::BM;
+    const int wq = warp & 3;
+    const int row = wq * 32 + (int)lane_id();
+    const int tid = (int)threadIdx.x;
+    const bool issuer = (tid == 128);
+    const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
+    const int c_lo = warp < 4 ? kLB / 2 : 0;
+    const int slice = row / R;
+    const int tile = (erow / C::BM) * (args.L / kLB) + u.l0 / kLB;
+    constexpr int kChunks = kLB / 4;  // 16-byte column chunks per row
+    // exchange region of (tile, split s): [kChunks][128 rows] x 16 B
+    auto region = [&](int s_) { return args.slab + ((size_t)tile * S + s_) * (kChunks * 128 * 4); };
+    auto slab_flag = [&](int s_) { return args.flags + (1u << 17) + tile * 16 + s_; };
+    mbar_wait_cluster(e_full, (my_units - 1) & 1);
+    __syncwarp();  // warps 0/1 arrive from divergent role loops; tcgen05.ld is warp-collective
+    tc_fence_after();
+    if (issuer) FF_STAMP(30);
+    // shared memory (drained stages): slot s = [kChunks][R rows][16 B] partial of split s
+    // for this split's rows (own partial staged from TMEM, partners' by TMA), then
+    // the bf16 E rows [kLB/64][R][128 B] (SW128) for one TMA store
+    const uint32_t slot0 = base;
+    const uint32_t ebuf = base + S * R * kChunks * 16;
+    {
+      float* const dst = region(sp) + row * 4;
+      const uint32_t own = slot0 + sp * (R * kChunks * 16) + (row - sp * R) * 16;
+#pragma unroll 1
+      for (int c0 = c_lo; c0 < c_lo + kLB / 2; c0 += 64) {
+        float v[32], w[32];
+        tmem_ld32x2(lane_base + C::kTMEM_E + c0, lane_base + C::kTMEM_E + c0 + 32, v, w);
+        if (slice != sp) {  // another split's row: straight to this split's exchange region
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            st_global_v4(dst + (size_t)(c0 / 4 + j) * 512, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            st_global_v4(dst + (size_t)(c0 / 4 + 8 + j) * 512, __float_as_uint(w[4 * j]),
+                         __float_as_uint(w[4 * j + 1]), __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
+          }
+        } else {  // own row: shared-memory slot sp
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            st_shared_v4(own + (c0 / 4 + j) * (R * 16), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            st_shared_v4(own + (c0 / 4 + 8 + j) * (R * 16), __float_as_uint(w[4 * j]), __float_as_uint(w[4 * j + 1]),
+                         __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
+          }
+        }
+      }
+      if (slice != sp) __threadfence();
+    }
+    __syncthreads();
+    if (issuer) {
+      FF_STAMP(24);
+      st_release_gpu_u32(slab_flag(sp), args.epoch);
+      if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
+      uint32_t polls = 0;
+      for (int j = 0; j < S; ++j) {
+        if (j == sp) continue;
+        while ((int)(ld_relaxed_gpu_u32(slab_flag(j)) - args.epoch) < 0)
+          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+      }
+      fence_acq_rel_gpu();
+      fence_proxy_async_global();
+      if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 27] = globaltimer_ns();
+      mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kChunks * 16));
+      for (int j = 0; j < S; ++j)
+        if (j != sp)
+          tma_load_3d(slot0 + j * (R * kChunks * 16), &maps.slab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
+    }
+    mbar_wait(e_load, 0);
+    if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 28] = globaltimer_ns();
+    // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
+    const uint8_t* const src = smem_gen;
+    const int n_items = (args.dbg & 32u) ? 0 : R * kChunks;  // diagnostics: skip the sum
+#pragma unroll 1
+    for (int it0 = tid; it0 < n_items; it0 += 1024) {
+      float4 acc[4];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) acc[q4] = *reinterpret_cast<const float4*>(src + (it0 + 256 * q4) * 16);
+#pragma unroll 1
+      for (int j = 1; j < S; ++j) {
+        float4 f[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          f[q4] = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + (it0 + 256 * q4) * 16);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          acc[q4].x += f[q4].x;
+          acc[q4].y += f[q4].y;
+          acc[q4].z += f[q4].z;
+          acc[q4].w += f[q4].w;
+        }
+      }
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int it = it0 + 256 * q4;
+        const int c = it / R, rr = it % R;
+        const int ch = (c % 16) / 2;
+        *reinterpret_cast<uint2*>(smem_gen + (ebuf - base) + (c / 16) * (R * 128) + rr * 128 + ((ch ^ (rr & 7)) << 4) +
+                                  (c & 1) * 8) =
+            make_uint2(pack_bf16x2(acc[q4].x, acc[q4].y), pack_bf16x2(acc[q4].z, acc[q4].w));
+      }
+    }
+    if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 22] = globaltimer_ns();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (issuer) {
+      tma_store_3d(&maps.er, ebuf, 0, erow + sp * R, u.l0 / 64);
+      bulk_commit();
+      FF_STAMP(26);
+      bulk_wait_read0();
     }
   }
 
