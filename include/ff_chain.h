@@ -88,7 +88,9 @@ typedef struct ffKernelConfig {
   int32_t steps;       /* derived: n-steps per split */
   int32_t units;       /* derived: m_tiles * l_clusters * n_splits work units */
   int32_t rings;       /* derived: co-resident rings launched (persistent over units) */
-  int32_t grid_ctas;   /* derived: rings * ring */
+  int32_t grid_ctas;   /* derived: CTAs launched (rings * ring * CTAs per member, + 2 * helpers) */
+  int32_t helpers;     /* derived (pair kernel): helper CTA pairs on the SMs the rings leave idle */
+  int32_t helper_x;    /* derived (pair kernel): last hops of every member n-step run by the helpers */
 } ffKernelConfig;
 
 /* Tensors: row-major, the reference layouts (simulator.py:112-123):

@@ -97,6 +97,8 @@ class KernelConfig(ctypes.Structure):
         ("units", ctypes.c_int32),
         ("rings", ctypes.c_int32),
         ("grid_ctas", ctypes.c_int32),
+        ("helpers", ctypes.c_int32),
+        ("helper_x", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

@@ -205,6 +205,45 @@ std::atomic<uint32_t> g_epoch{0};
 unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
 uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
 
+// Split-N finish by exchange regions (pair kernel): one unit per ring, S | 128
+// with 8-row slices, and the slab flags of every E tile fit their region.
+bool pair_finish_regions(const ffChainDesc* ch, const ffKernelConfig* c, int rings) {
+  return c->n_splits > 1 && c->n_splits <= 8 && c->units <= rings && 128 % c->n_splits == 0 &&
+         (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 <= (1u << 17);
+}
+
+// Helper pairs (pair kernel) on the SMs a split-N launch leaves idle: they take
+// the last x hops of every member n-step.  x balances the members' work
+// (steps GEMM0 chunks of r hop-times each + steps*(G-x) hops) against the
+// helpers' (about one chunk of r hop-times waiting for the first published C,
+// then steps*units*G*x/H hops); the NS = m_tiles*G*steps segments are dealt out
+// in contiguous blocks.  Two n-steps at most: the helper zone then
+// sums two partials into zero, which is order-independent.
+void plan_helpers(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
+  c->helpers = 0;
+  c->helper_x = 0;
+  // Opt-in (measured slower, profiles/r01/helper_x.log): the fused chain at 128 SMs is
+  // already bound by the chip's aggregate operand feed; the helpers' extra hops slow
+  // the members' hops by as much as they add.  FF_HELPERS=1 or debug bit 26 enables.
+  static const bool env_on = std::getenv("FF_HELPERS") != nullptr;
+  if (c->exchange != FF_XCHG_L2_PAIR || (g_dbg & (1u << 24)) || !(env_on || (g_dbg & (1u << 26)))) return;
+  if (!pair_finish_regions(ch, c, c->rings) || c->steps > 2 || c->l_clusters != 1) return;
+  const int H = (num_sms - c->rings * c->ring * 2) / 2;
+  if (H < 1) return;
+  if ((size_t)c->steps * c->m_tiles * 256 * ch->l * sizeof(float) > kEZoneBytes) return;  // helper regions
+  const double r = (double)ch->k / (ch->kind == FF_KIND_GATED ? 128 : 256);
+  const double G = c->ring, st = c->steps, units = c->units;
+  // members: st*r + st*(G - x) hop-times; helpers: r + 2 (first chunks drained and
+  // published) + st*x*units*G/H
+  int x = (int)std::lround((st * r + st * G - r - 2) / (st * (1.0 + units * G / H)));
+  if ((g_dbg >> 16) & 15u) x = (int)((g_dbg >> 16) & 15u) - 1;
+  x = std::min(x, c->ring - 2);
+  if (x < 1) return;
+  c->helpers = H;
+  c->helper_x = x;
+}
+
+
 template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
                 void* c_debug, cudaStream_t stream, const ffConvDesc* conv) {
@@ -286,6 +325,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
+  a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
   if (implicit) {
     a.conv_k1 = conv->k1;
     a.conv_H = conv->h;
@@ -388,6 +428,9 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const uint64_t ds[3] = {32, 16, tiles * S * 64}, ss[2] = {128, 2048};
     const uint32_t bs[3] = {32, rs / 8, 64};
     ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sp, ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const uint64_t dz[3] = {32, 16, tiles * 64};
+    ok = ok && make_map_nd(&maps.hz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, wsb + wl.e_off, dz, ss, bs,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
   }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
@@ -424,11 +467,16 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
   a.defer = cfg->ring - 1 - cfg->ring / 4;  // measured: 3/4 of the hops (profiles/r01/cfgs_defer.log)
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
-  a.finish_tma = cfg->n_splits > 1 && cfg->n_splits <= 8 && cfg->units <= rings && 128 % cfg->n_splits == 0 &&
-                 (128 / cfg->n_splits) % 8 == 0 &&
-                 (size_t)((M + 255) / 256) * 2 * (L / 256) * 16 <= (1u << 17);
+  a.finish_tma = pair_finish_regions(ch, cfg, rings);
+  // helper pairs (planned by finish_config for the non-quad launch)
+  a.helpers = (!kQuad && rings == cfg->rings) ? cfg->helpers : 0;
+  a.helper_x = a.helpers > 0 ? cfg->helper_x : 0;
+  a.hzone = reinterpret_cast<float*>(wsb + wl.e_off);
   if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);
   a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
+  // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
+  // debug bit 27 restores the common order
+  a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
   a.defer_last = (g_dbg & 128u) ? 0 : 1;
   if ((g_dbg >> 12) & 15u) a.prefetch = (int)((g_dbg >> 12) & 15u) - 1;
   if (wl.e_memset) {
@@ -436,7 +484,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(rings * cfg->ring * 2, 1, 1);
+  lc.gridDim = dim3(rings * cfg->ring * 2 + 2 * a.helpers, 1, 1);
   lc.blockDim = dim3(256, 1, 1);
   lc.dynamicSmemBytes = C::kSMEM;
   lc.stream = stream;
@@ -469,6 +517,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
 // at most one unit each... any even ring count works (units 2j / 2j+1 pair up).
 bool quad_ok(const ffKernelConfig* cfg) {
   if (g_dbg & 64u) return false;  // diagnostics: force the plain pair kernel
+  if (cfg->helpers > 0) return false;  // helper pairs fill the SMs a cluster-of-4 launch cannot
   if (cfg->m_tiles % 2 || cfg->units % 2) return false;
   int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
   rings = std::min(rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring));
@@ -558,7 +607,8 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const int64_t max_rings =
       c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
   c->rings = (int32_t)std::min<int64_t>(units, max_rings);
-  c->grid_ctas = c->rings * c->ring * width;
+  plan_helpers(ch, c, num_sms);
+  c->grid_ctas = c->rings * c->ring * width + 2 * c->helpers;
   return FF_OK;
 }
 

@@ -62,10 +62,14 @@ struct ChainArgs {
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
   float* slab;         // pair kernel: split-N exchange regions [E tile][split][16-B chunk][128 rows]
+  int helpers;         // pair kernel: helper pairs on the SMs the rings leave idle (0 = none)
+  int helper_x;        // pair kernel: last hops of every member's n-steps executed by the helpers
+  float* hzone;        // pair kernel: helper E partials, [E tile][16-B chunk][128 rows], zero between launches
   uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
   int defer;           // pair kernel: hops of step T that run after GEMM0(T+1) (< G)
   int defer_last;      // pair kernel: run the ring's last GEMM0 before all hops of the previous step
+  int krot;            // pair kernel: rotate each member's GEMM0 k order by its ring position
   int prefetch;        // pair kernel: L2 prefetch distance for weight tiles (k-blocks / hops), 0 = off
   int finish_tma;      // pair kernel: split finish by bulk copies (one unit per ring, 128/S % 8 == 0)
   // conv chain as implicit GEMM (conv_k1 > 1): A is an NHWC feature map read
@@ -79,9 +83,11 @@ struct ChainArgs {
 
 #define FF_PROF_STRIDE 32
 // Stamp timeline slot `i` (16..31) of this CTA with the global nanosecond timer.
+// Profile row of this CTA (the pair kernel redefines it to its virtual CTA index).
+#define FF_PROF_ROW blockIdx.x
 #define FF_STAMP(i)                                                        \
   do {                                                                     \
-    if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + (i)] = globaltimer_ns(); \
+    if (args.prof) args.prof[(FF_PROF_ROW) * FF_PROF_STRIDE + (i)] = globaltimer_ns(); \
   } while (0)
 // Accumulate the cycles spent in `stmt` into `acc` when profiling is on.
 #define FF_TIMED(acc, stmt)                                           \
@@ -247,6 +253,9 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t p = kDSM ? cluster_rank() : (uint32_t)(blockIdx.x % G);  // ring position
   const int ring = blockIdx.x / G;
   const int kblocks = args.K / C::BK;
+  // GEMM0 k order rotated by ring position (members of a ring and the rings of
+  // an m tile would otherwise request the same A box at the same moment)
+  const int krot = args.krot ? ((int)p * kblocks / G) : 0;
   const int steps = args.steps;
   // units processed by this ring; the flat list of (unit, n-step) is the "global step" T
   const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
@@ -339,7 +348,8 @@ __global__ void __launch_bounds__(256, 1)
       auto load_gemm0 = [&](int T, int kb0, int kb1) {
         const Unit u = unit_of(T / steps);
         const int n0 = u.n0 + ((T % steps) * G + (int)p) * kNB;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kbl = kb0; kbl < kb1; ++kbl) {
+          const int kb = (kbl + krot) % kblocks;  // staggered k order across ring members
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);

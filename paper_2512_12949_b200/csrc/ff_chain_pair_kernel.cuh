@@ -37,6 +37,7 @@ struct PairMaps {
   CUtensorMap e3;   // E bf16 3D {64, M, L/64}, box {64, 128, kLB/64}
   CUtensorMap w3;   // fp32 workspace 3D {32, M, L/32}, box {32, 128, kLB/32}
   CUtensorMap er;   // E bf16 3D, box {64, 128/S, kLB/64}: one row slice of a tile
+  CUtensorMap hz;   // helper zone, same geometry as slab (S = 1)
   CUtensorMap slab; // split-N exchange regions 3D {32, 16, tiles*S*64} fp32, box {32, 128/S/8, 64} (no swizzle)
 };
 
@@ -72,6 +73,8 @@ struct PairCfg {
 // TMA instructions per two stages per CTA instead of four (the TMA unit is
 // per-instruction bound: profiles/r01/mcast_relaxed.log).  Stages are freed
 // by both leaders' commits (empty-barrier count 2, commit mask 0xF).
+#undef FF_PROF_ROW
+#define FF_PROF_ROW vcta
 template <bool kGated, int kLB, int kStages, bool kPackedB, bool kQuad>
 __global__ void __launch_bounds__(256, 1)
     ff_chain_pair_kernel(const __grid_constant__ PairMaps maps, const ChainArgs args) {
@@ -81,7 +84,6 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
-  if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;                  // ring members (pairs)
   const uint32_t crank = cluster_rank();
@@ -89,12 +91,32 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t pq = kQuad ? crank >> 1 : 0u;  // pair within the quad (0 = X, 1 = Y)
   const uint32_t lrank = 2u * pq;        // this pair's leader rank in the cluster
   const bool leader = (q == 0);
-  const int p = kQuad ? (int)(blockIdx.x / 4) % G : (int)(blockIdx.x / 2) % G;  // ring position
-  const int ring = kQuad ? 2 * ((int)(blockIdx.x / 4) / G) + (int)pq : (int)(blockIdx.x / 2) / G;
+  // Helper pairs are spread over the grid (every `stride`-th pair) rather than
+  // appended: consecutive clusters fill a GPC, and 20 streaming helper SMs in
+  // one or two GPCs starve on the GPC's share of L2 bandwidth.  Virtual CTA
+  // index: members 0..member_ctas-1 in ring order, then the helpers.
+  const int member_ctas = args.n_rings * G * 2;
+  int vcta = (int)blockIdx.x;
+  if (!kQuad && args.helpers > 0) {
+    const int pi = (int)blockIdx.x / 2, H = args.helpers, stride = (member_ctas / 2 + H) / H;
+    if (pi % stride == stride - 1 && pi / stride < H)
+      vcta = member_ctas + 2 * (pi / stride) + (int)q;
+    else
+      vcta = 2 * (pi - min(H, (pi + 1) / stride)) + (int)q;
+  }
+  if (threadIdx.x == 0) FF_STAMP(16);
+  const int p = kQuad ? (vcta / 4) % G : (vcta / 2) % G;  // ring position
+  const int ring = kQuad ? 2 * ((vcta / 4) / G) + (int)pq : (vcta / 2) / G;
   const uint16_t mcast = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));  // this CTA and its twin
   const int kblocks = args.K / C::BK;
+  // GEMM0 k order rotated by ring position: the 2*G*S CTAs of an m tile would
+  // otherwise request the same A box at the same moment (one L2 slice set)
+  const int krot = args.krot ? (p * kblocks / G) : 0;
   const int steps = args.steps;
-  const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
+  const bool is_helper = vcta >= member_ctas;
+  const int hx = args.helpers > 0 ? args.helper_x : 0;     // hops per member n-step left to the helpers
+  const int my_units =
+      (!is_helper && ring < args.n_units) ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
   const int total_steps = my_units * steps;
 
   struct Unit {
@@ -167,8 +189,206 @@ __global__ void __launch_bounds__(256, 1)
   // Split-N reduce-scatter tail (one unit per ring, S > 1): all eight warps
   // drain the ring's last E partial after the role loops (see below).
   const bool scatter_all = args.S > 1 && args.finish_tma && total_steps > 0;
+  // A tile: two K-major [128 x 64] SW128 tiles; B tile: MN-major [128 k x 64] tiles 16 KB apart
+  auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
+  auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
+  constexpr int kChunks = kLB / 4;  // 16-byte column chunks per E row
 
-  if (warp == 0) {
+  if (is_helper) {
+    // ===================== helper pair (SMs the rings leave idle) =====================
+    // A segment = (n-step t, m tile, member position p): the last hx hops of
+    // n-step t of member p in every N split's ring of that m tile (chunks of
+    // origins (p-h) mod G, h >= G-hx), which those members skip.  All of them
+    // accumulate into one TMEM E buffer (two buffers, alternating), drained by
+    // plain stores into the helper region (E tile, t); the members add the
+    // regions of every n-step, in order, in their split-N reduce-scatter
+    // (bit-reproducible: no atomics).
+    // Segments are listed position-major (p, m tile, then t); helper hp owns the
+    // contiguous block [hp*NS/H, (hp+1)*NS/H) and runs its step-0 segments first
+    // (their chunks are published first), then its step-1 segments.
+    const int H = args.helpers;
+    const int hp = (vcta - member_ctas) / 2;
+    const int NS = args.m_tiles * G * steps;
+    const int s_lo = (int)((long long)hp * NS / H), s_hi = (int)((long long)(hp + 1) * NS / H);
+    const int n_seg = s_hi - s_lo;
+    struct Seg {
+      int t, mt, p;
+    };
+    auto seg_of = [&](int i) {  // i-th segment in execution order
+      int sg = s_lo, t = 0;
+      for (t = 0; t < steps; ++t) {
+        const int first = s_lo + ((t - s_lo % steps) % steps + steps) % steps;  // first sg in range with sg%steps==t
+        const int cnt = first < s_hi ? (s_hi - 1 - first) / steps + 1 : 0;
+        if (i < cnt) {
+          sg = first + i * steps;
+          break;
+        }
+        i -= cnt;
+      }
+      const int mp = sg / steps;  // positions p-major: both m tiles of a p read the same D rows
+      return Seg{t, mp % args.m_tiles, mp / args.m_tiles};
+    };
+    auto unit_at = [&](const Seg& g, int split) {  // l_clusters == 1
+      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * steps * G * C::kN0, g.mt + args.m_tiles * split, split};
+    };
+    const uint32_t hb_full[2] = {e_full, c_full}, hb_empty[2] = {e_empty, c_empty};
+    if (warp == 0) {
+      if (elect_one()) {
+        int stage = 0, phase = 0;
+        unsigned long long w_empty = 0, w_flag = 0;
+        const unsigned long long t_start = clock64();
+        const int nh = args.S * hx;  // hops per segment
+        auto hop_at = [&](const Seg& g, int hs, Unit& u, int& origin) {
+          u = unit_at(g, hs / hx);
+          origin = (g.p - (G - hx + hs % hx) + G) % G;
+        };
+        for (int i = 0; i < n_seg; ++i) {
+          const Seg g = seg_of(i);
+          const int dblk = g.p * kLB / 64 + (int)q * (kLB / 128);
+          // wait for every chunk of the segment at once: one round trip polls all
+          // missing flags (they are published together, at the end of GEMM0(t))
+          {
+            unsigned long long ready = 0ull;
+            const unsigned long long all = nh >= 64 ? ~0ull : (1ull << nh) - 1ull;
+            uint32_t polls = 0;
+            const unsigned long long tf0 = args.prof ? clock64() : 0ull;
+            while (ready != all) {
+              for (int h0 = 0; h0 < nh; h0 += 8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  v[j] = args.epoch;
+                  if (h0 + j < nh && !((ready >> (h0 + j)) & 1ull)) {
+                    Unit u;
+                    int origin;
+                    hop_at(g, h0 + j, u, origin);
+                    v[j] = ld_relaxed_gpu_u32(flag_addr(u, g.t, origin, (int)q));
+                  }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (h0 + j < nh && (int)(v[j] - args.epoch) >= 0) ready |= 1ull << (h0 + j);
+              }
+              if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+            }
+            if (args.prof) w_flag += clock64() - tf0;
+            fence_acq_rel_gpu();
+            fence_proxy_async_global();
+          }
+          for (int hs = 0; hs < nh; ++hs) {
+            Unit u;
+            int origin;
+            hop_at(g, hs, u, origin);
+            const int ncol0 = u.n0 + (g.t * G + origin) * C::kN0;
+            if (hs + 2 < nh) {  // D rows two hops ahead into L2 (weights stream from HBM)
+              Unit u2;
+              int o2;
+              hop_at(g, hs + 2, u2, o2);
+              const int nc2 = u2.n0 + (g.t * G + o2) * C::kN0;
+              for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) tma_prefetch_l2_3d(&maps.d, 0, nc2 + kb2 * C::BK, dblk);
+            }
+            for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+              FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
+              const uint32_t sb = base + stage * C::kSTAGE;
+              const uint32_t lb = mapa(full_bar(stage), lrank);
+              if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
+              tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
+              tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
+              if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+          }
+        }
+        if (args.prof) {
+          unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
+          pr[0] = clock64() - t_start;
+          pr[1] = w_empty;
+          pr[2] = w_flag;
+        }
+      }
+    } else if (warp == 1) {
+      if (leader && elect_one()) {
+        constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
+        int stage = 0, phase = 0;
+        unsigned long long w_full = 0, w_buf = 0;
+        const unsigned long long t_start = clock64();
+        for (int i = 0; i < n_seg; ++i) {
+          const int eb = i & 1;
+          if (i >= 2) {
+            FF_TIMED(w_buf, mbar_wait_cluster(hb_empty[eb], ((i >> 1) - 1) & 1));
+            tc_fence_after();
+          }
+          bool started = false;
+          for (int hs = 0; hs < args.S * hx; ++hs) {
+            for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+              FF_TIMED(w_full, mbar_wait(full_bar(stage), phase));
+              tc_fence_after();
+              const uint32_t sb = base + stage * C::kSTAGE;
+#pragma unroll
+              for (int kk = 0; kk < C::BK / 16; ++kk) {
+                umma_bf16_pair(tmem_base + eb * C::kTMEM_E, a_desc(sb, kk), b_desc(sb + C::kSLOT, kk), idesc1,
+                               started ? 1u : 0u);
+                started = true;
+              }
+              umma_commit_pair(empty_bar(stage), kPairMask);
+              if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+          }
+          umma_commit_pair(hb_full[eb], kPairMask);
+        }
+        if (args.prof) {
+          unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
+          pr[3] = clock64() - t_start;
+          pr[4] = w_full;
+          pr[8] = w_buf;
+        }
+      }
+    } else if (warp >= 4) {
+      const int wq = warp & 3;
+      const int row = wq * 32 + (int)lane_id();
+      const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
+      for (int i = 0; i < n_seg; ++i) {
+        const int eb = i & 1;
+        mbar_wait_cluster(hb_full[eb], (i >> 1) & 1);
+        tc_fence_after();
+        if (warp == 4 && lane_id() == 0 && i < 6) FF_STAMP(18 + i);  // diagnostics: segment i's MMAs done
+        const Seg g = seg_of(i);
+        const int erow = g.mt * 2 * C::BM + (int)q * C::BM;
+        const int tile = (erow / C::BM) * (args.L / kLB) + g.p;
+        // plain coalesced stores into the segment's own region (tile, t): a warp's
+        // 32 rows of one 16-byte column chunk are 512 contiguous bytes
+        float* const dst = args.hzone + ((size_t)tile * steps + g.t) * (kChunks * 128 * 4) + row * 4;
+        const int c_end = (args.dbg & (1u << 25)) ? 0 : kLB;  // diagnostics: skip the drain
+#pragma unroll 1
+        for (int c0 = 0; c0 < c_end; c0 += 64) {
+          float v[32], w[32];
+          tmem_ld32x2(lane_base + eb * C::kTMEM_E + c0, lane_base + eb * C::kTMEM_E + c0 + 32, v, w);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            st_global_v4(dst + (size_t)(c0 / 4 + j) * 512, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            st_global_v4(dst + (size_t)(c0 / 4 + 8 + j) * 512, __float_as_uint(w[4 * j]), __float_as_uint(w[4 * j + 1]),
+                         __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
+          }
+        }
+        // TMEM buffer free: tcgen05 loads waited + fenced; the arrive publishes no data
+        tc_fence_before();
+        mbar_arrive_remote_relaxed(mapa(hb_empty[eb], lrank));
+        // region complete: the barrier orders the 128 threads' stores before the
+        // issuer's gpu-scope release (cumulative), no per-thread fence
+        named_bar_sync(1, 128);
+        if (warp == 4 && lane_id() == 0) {
+          red_add_release_gpu_u32(args.tile_cnt + tile, 1u);
+          if (i < 6) FF_STAMP(24 + i);  // diagnostics: segment i drained
+        }
+      }
+    }
+  } else if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (elect_one()) {
       unsigned long long w_empty = 0, w_flag = 0;
@@ -194,7 +414,8 @@ __global__ void __launch_bounds__(256, 1)
         const Unit u = unit_of(T / steps);
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
         const int nblk = (u.n0 + ((T % steps) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kbl = kb0; kbl < kb1; ++kbl) {
+          const int kb = (kbl + krot) % kblocks;  // physical k-block (members start at staggered k)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
@@ -204,11 +425,12 @@ __global__ void __launch_bounds__(256, 1)
           // L2 prefetch of the B tile `prefetch` k-blocks ahead: the weights
           // stream from HBM; the extra lead hides its latency behind 3 stages
           const int pf = args.prefetch;
-          if (pf && kb + pf < kblocks && (!kQuad || pq == 0)) {
+          if (pf && kbl + pf < kblocks && (!kQuad || pq == 0)) {
+            const int kbp = (kbl + pf + krot) % kblocks;
             if (!kGated || !kPackedB)
-              tma_prefetch_l2_3d(&maps.b, 0, (kb + pf) * C::BK, nblk);
+              tma_prefetch_l2_3d(&maps.b, 0, kbp * C::BK, nblk);
             else
-              tma_prefetch_l2_4d(&maps.b, 0, (kb + pf) * C::BK, nblk, 0);
+              tma_prefetch_l2_4d(&maps.b, 0, kbp * C::BK, nblk, 0);
           }
           if (!mine) {
           } else if (kQuad) {
@@ -281,11 +503,11 @@ __global__ void __launch_bounds__(256, 1)
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
           if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          load_hop(T, h);
+          if (h < G - hx) load_hop(T, h);  // the last hx hops run on the helpers
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
+        unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
         pr[0] = clock64() - t_start;
         pr[1] = w_empty;
         pr[2] = w_flag;
@@ -305,9 +527,6 @@ __global__ void __launch_bounds__(256, 1)
       };
       constexpr uint32_t idesc0 = idesc_bf16(256, C::kN0, 0, 1);
       constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
-      // A tile: two K-major [128 x 64] SW128 tiles; B tile: MN-major [128 k x 64] tiles 16 KB apart
-      auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
-      auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
       auto gemm0 = [&](int T, int kb0, int kb1) {
         if (kb0 >= kb1) return;
         if (kb0 == 0) {
@@ -364,17 +583,17 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
         if (C::kOwnFull && h == 0) umma_commit_pair(own_free, kPairMask);
-        if (t == steps - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
+        if (t == steps - 1 && h == G - 1 - hx) umma_commit_pair(e_full, kPairMask);
       };
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
           if (T + 1 < total_steps) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          hop(T, h);
+          if (h < G - hx) hop(T, h);
         }
       }
       if (args.prof) {
-        unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
+        unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
         pr[3] = clock64() - t_start;
         pr[4] = w_full0;
         pr[5] = w_full1;
@@ -576,7 +795,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     if (issuer) bulk_wait_read0();  // smem sources of the E stores read before exit (writes drain at grid end)
     if (args.prof && issuer) {
-      unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
+      unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
       pr[9] = clock64() - t_start;
       pr[10] = w_cfull;
       pr[11] = w_ofree;
@@ -609,7 +828,6 @@ __global__ void __launch_bounds__(256, 1)
     const int c_lo = warp < 4 ? kLB / 2 : 0;
     const int slice = row / R;
     const int tile = (erow / C::BM) * (args.L / kLB) + u.l0 / kLB;
-    constexpr int kChunks = kLB / 4;  // 16-byte column chunks per row
     // exchange region of (tile, split s): [kChunks][128 rows] x 16 B
     auto region = [&](int s_) { return args.slab + ((size_t)tile * S + s_) * (kChunks * 128 * 4); };
     auto slab_flag = [&](int s_) { return args.flags + (1u << 17) + tile * 16 + s_; };
@@ -653,33 +871,51 @@ __global__ void __launch_bounds__(256, 1)
     if (issuer) {
       FF_STAMP(24);
       st_release_gpu_u32(slab_flag(sp), args.epoch);
-      if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
+      if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 25] = globaltimer_ns();
       uint32_t polls = 0;
       for (int j = 0; j < S; ++j) {
         if (j == sp) continue;
         while ((int)(ld_relaxed_gpu_u32(slab_flag(j)) - args.epoch) < 0)
           if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
       }
+      if (hx > 0)  // every helper segment (one per n-step) of this tile is in its region
+        while ((int)(ld_relaxed_gpu_u32(args.tile_cnt + tile) - (uint32_t)steps) < 0)
+          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
       fence_acq_rel_gpu();
       fence_proxy_async_global();
-      if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 27] = globaltimer_ns();
+      if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 27] = globaltimer_ns();
       mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kChunks * 16));
       for (int j = 0; j < S; ++j)
         if (j != sp)
           tma_load_3d(slot0 + j * (R * kChunks * 16), &maps.slab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
     }
     mbar_wait(e_load, 0);
-    if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 28] = globaltimer_ns();
+    if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
     // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
     const uint8_t* const src = smem_gen;
     const int n_items = (args.dbg & 32u) ? 0 : R * kChunks;  // diagnostics: skip the sum
+    // helper regions (tile, t) of this slice's rows: coalesced global loads (item -> 16 B,
+    // consecutive threads -> consecutive rows of one column chunk)
+    const float* const hreg = args.hzone + (size_t)tile * steps * (kChunks * 128 * 4) + sp * R * 4;
 #pragma unroll 1
     for (int it0 = tid; it0 < n_items; it0 += 1024) {
+      float4 hv[2][4];
+      if (hx > 0) {
+#pragma unroll
+        for (int t2 = 0; t2 < 2; ++t2)
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int it = it0 + 256 * q4;
+            hv[t2][q4] = t2 < steps ? ld_global_f4(hreg + (size_t)t2 * (kChunks * 128 * 4) + (size_t)(it / R) * 512 +
+                                                   (it % R) * 4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+      }
       float4 acc[4];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) acc[q4] = *reinterpret_cast<const float4*>(src + (it0 + 256 * q4) * 16);
 #pragma unroll 1
-      for (int j = 1; j < S; ++j) {
+      for (int j = 1; j < S; ++j) {  // splits in order
         float4 f[4];
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
@@ -692,6 +928,18 @@ __global__ void __launch_bounds__(256, 1)
           acc[q4].w += f[q4].w;
         }
       }
+      if (hx > 0) {  // then the helpers' n-step partials, in order
+#pragma unroll
+        for (int t2 = 0; t2 < 2; ++t2)
+          if (t2 < steps)
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              acc[q4].x += hv[t2][q4].x;
+              acc[q4].y += hv[t2][q4].y;
+              acc[q4].z += hv[t2][q4].z;
+              acc[q4].w += hv[t2][q4].w;
+            }
+      }
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         const int it = it0 + 256 * q4;
@@ -702,13 +950,15 @@ __global__ void __launch_bounds__(256, 1)
             make_uint2(pack_bf16x2(acc[q4].x, acc[q4].y), pack_bf16x2(acc[q4].z, acc[q4].w));
       }
     }
-    if (issuer && args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 22] = globaltimer_ns();
+    if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 22] = globaltimer_ns();
     fence_proxy_async_smem();
     __syncthreads();
     if (issuer) {
       tma_store_3d(&maps.er, ebuf, 0, erow + sp * R, u.l0 / 64);
       bulk_commit();
       FF_STAMP(26);
+      if (hx > 0 && atom_add_acqrel_gpu_u32(args.tile_cnt + tile, 1u) == (uint32_t)(steps + S - 1))
+        *reinterpret_cast<volatile uint32_t*>(args.tile_cnt + tile) = 0u;  // all splits past their wait
       bulk_wait_read0();
     }
   }
@@ -721,5 +971,8 @@ __global__ void __launch_bounds__(256, 1)
     tmem_dealloc_pair<512>(tmem_base);
   }
 }
+
+#undef FF_PROF_ROW
+#define FF_PROF_ROW blockIdx.x
 
 }  // namespace ff

@@ -21,7 +21,7 @@ for name in sel:
     for _ in range(3): f()
     runs = []
     for it in range(5):
-        flush_buf.add_(1.0)
+        if 'warm' not in ARGV: flush_buf.add_(1.0)
         ea = torch.cuda.Event(enable_timing=True); eb = torch.cuda.Event(enable_timing=True)
         buf.zero_()
         lib.ff_set_profile_buffer(ctypes.c_void_p(buf.data_ptr())); ea.record(); f(); eb.record(); lib.ff_set_profile_buffer(None)
@@ -47,3 +47,23 @@ for name in sel:
             cols = {k: blk[:, i] for i, k in ((2, 'cfull0'), (5, 'cfull1'), (14, 'E_start'), (15, 'exit'))}
             print("   ring %d: " % r + " ".join(f"{k} {c[~torch.isnan(c)].mean().item():6.1f}/{c[~torch.isnan(c)].max().item():6.1f}" for k, c in cols.items()))
 lib.ff_set_debug_mode(0)
+# helper segment completion stamps (slots 18.. of the helper CTAs)
+if 'helpers' in ARGV:
+    for name in sel:
+        A,B,B1,D,E,ch,kc,ws,t = setup(*SHAPES[name],None,2)
+        if kc.helpers == 0: continue
+        f=lambda: nat.check(lib.ff_chain_launch(ctypes.byref(ch),ctypes.byref(kc),ctypes.byref(t),ws.data_ptr(),ws.numel(),None))
+        buf = torch.zeros(kc.grid_ctas*ST + 64, dtype=torch.int64, device='cuda')
+        for _ in range(3): f()
+        if 'warm' not in ARGV: flush_buf.add_(1.0)
+        buf.zero_()
+        lib.ff_set_profile_buffer(ctypes.c_void_p(buf.data_ptr())); f(); lib.ff_set_profile_buffer(None)
+        torch.cuda.synchronize()
+        v = buf[:kc.grid_ctas*ST].view(kc.grid_ctas, ST)[:, 16:].double()
+        t0 = v[:kc.grid_ctas - 2*kc.helpers, 0].min()
+        for hcta in range(kc.grid_ctas - 2*kc.helpers, kc.grid_ctas, 2):
+            row = v[hcta]
+            segs = [f"{(a - t0).item()/1e3:6.1f}/{(b - t0).item()/1e3:6.1f}" for a, b in zip(row[2:8], row[8:14]) if a > 0]
+            print(f"   helper cta {hcta}: entry {(row[0]-t0).item()/1e3:5.1f} segs mma-done/drained {' '.join(segs)}")
+            cnt = buf[:kc.grid_ctas*ST].view(kc.grid_ctas, ST)[hcta, :16].double() / 1.965e3
+            print(f"      prod total {cnt[0]:.1f} w_empty {cnt[1]:.1f} w_flag {cnt[2]:.1f} | mma total {cnt[3]:.1f} w_full {cnt[4]:.1f} w_buf {cnt[8]:.1f} us")
