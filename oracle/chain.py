@@ -203,9 +203,18 @@ def conv_chain(x: np.ndarray, w1: np.ndarray, w2: np.ndarray, activation: str = 
                bf16_intermediate: bool = False) -> np.ndarray:
     """conv(k1 x k1, same) -> act -> conv(1x1) as the GEMM chain the reference
     executes on a conv preset (dense_chain over the im2col matrix).
-    x [b, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2] -> y [b, h, w, oc2]."""
+    x [b, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2] -> y [b, h, w, oc2].
+    Extension (no reference counterpart): w2 [k2, k2, oc1, oc2] applies a k2 x k2
+    second convolution to the intermediate (im2col of C, same padding)."""
     b, h, w, _ = x.shape
     k1 = w1.shape[0]
+    if w2.ndim == 4:
+        c = _ACT[activation](im2col_nhwc(x, k1) @ w1.reshape(-1, w1.shape[-1]))
+        if bf16_intermediate:
+            c = round_bf16(c)
+        c = c.reshape(b, h, w, w1.shape[-1])
+        y = im2col_nhwc(c, w2.shape[0]) @ w2.reshape(-1, w2.shape[-1])
+        return y.reshape(b, h, w, w2.shape[-1])
     inputs = {"A": im2col_nhwc(x, k1), "B": w1.reshape(-1, w1.shape[-1]), "D": w2}
     y = dense_chain("standard_ffn", activation, inputs, bf16_intermediate=bf16_intermediate)
     return y.reshape(b, h, w, w2.shape[1])

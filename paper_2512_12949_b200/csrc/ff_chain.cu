@@ -68,15 +68,15 @@ EncodeIm2colFn encode_im2col_fn() {
 // corners -pad / pad-(k1-1) make the traversal enumerate exactly the h x w
 // output positions; the tap offsets (s, r) then address the input pixel and
 // out-of-image taps read zeros.
-bool make_map_im2col(CUtensorMap* map, const void* ptr, const ffConvDesc* cv) {
+bool make_map_im2col(CUtensorMap* map, const void* ptr, int channels, int w, int h, int batch, int k) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return false;
-  const int pad = cv->k1 / 2;
-  cuuint64_t dims[4] = {(cuuint64_t)cv->ic, (cuuint64_t)cv->w, (cuuint64_t)cv->h, (cuuint64_t)cv->batch};
-  cuuint64_t strides[3] = {(cuuint64_t)cv->ic * 2, (cuuint64_t)cv->w * cv->ic * 2,
-                           (cuuint64_t)cv->h * cv->w * cv->ic * 2};
+  const int pad = k / 2;
+  cuuint64_t dims[4] = {(cuuint64_t)channels, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)channels * 2, (cuuint64_t)w * channels * 2,
+                           (cuuint64_t)h * w * channels * 2};
   int lower[2] = {-pad, -pad};
-  int upper[2] = {pad - (cv->k1 - 1), pad - (cv->k1 - 1)};
+  int upper[2] = {pad - (k - 1), pad - (k - 1)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, lower, upper, 64,
                   128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -86,7 +86,7 @@ bool make_map_im2col(CUtensorMap* map, const void* ptr, const ffConvDesc* cv) {
   // <= 13.1 on tensors below 128 KB (cute/atom/copy_traits_sm90_im2col.hpp).
   int drv = 0;
   if (cudaDriverGetVersion(&drv) == cudaSuccess && drv <= 13010 &&
-      (uint64_t)cv->batch * cv->h * cv->w * cv->ic * 2 < 131072)
+      (uint64_t)batch * h * w * channels * 2 < 131072)
     reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
   return true;
 }
@@ -178,13 +178,15 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr size_t kFlagBytes = 1u << 20;
 constexpr size_t kCntBytes = 256u << 10;
 constexpr size_t kEZoneBytes = 32u << 20;
-WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c) {
+WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = false) {
   WsLayout w{};
   const bool pair = c->exchange == FF_XCHG_L2_PAIR;
   const size_t e_bytes = c->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
   // C scratch: L2 transport with a ring > 1; the standard-FFN pair kernel also
   // reads its own chunk back from it (hop 0), so it always needs one.
-  const bool c_scratch = c->exchange != FF_XCHG_DSM && (c->ring > 1 || (pair && ch->kind != FF_KIND_GATED));
+  // (a k2 x k2 second convolution reads the whole intermediate back through im2col boxes)
+  const bool c_scratch =
+      c->exchange != FF_XCHG_DSM && (c->ring > 1 || conv2 || (pair && ch->kind != FF_KIND_GATED));
   w.f_off = 0;
   w.n_off = kFlagBytes;
   w.e_off = kFlagBytes + kCntBytes;
@@ -263,17 +265,24 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
   const uint64_t M = ch->m, N = ch->n, K = ch->k, L = ch->l;
-  const WsLayout wl = ws_layout(ch, cfg);
-  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
-  CUtensorMap mA, mB0, mB1, mD, mC;
   const bool implicit = conv != nullptr && conv->k1 > 1;
-  bool ok = implicit ? make_map_im2col(&mA, t->a, conv) : make_map(&mA, t->a, M, K, 64, 128);
+  const bool conv2 = conv != nullptr && conv->k2 > 1;  // k2 x k2 second conv: GEMM1 over im2col(C)
+  const WsLayout wl = ws_layout(ch, cfg, conv2);
+  uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
+  CUtensorMap mA, mB0, mB1, mD, mC, mCs;
+  bool ok = implicit ? make_map_im2col(&mA, t->a, conv->ic, conv->w, conv->h, conv->batch, conv->k1)
+                     : make_map(&mA, t->a, M, K, 64, 128);
   ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
   ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
-  ok = ok && make_map(&mD, t->d, N, L, 64, 64);
+  ok = ok && make_map(&mD, t->d, conv2 ? (uint64_t)conv->k2 * conv->k2 * N : N, L, 64, 64);
   const bool l2x = (kMode == ff::XCHG_L2 && cfg->ring > 1);
-  ok = ok && make_map(&mC, l2x ? (const void*)(wsb + wl.c_off) : t->a, l2x ? (uint64_t)cfg->m_tiles * 128 : M,
-                      l2x ? N : K, 64, 128);
+  const bool cs = l2x || conv2;  // C scratch in use: [m_tiles*128][N] 2D view (publish stores, ring hops)
+  ok = ok && make_map(&mCs, cs ? (const void*)(wsb + wl.c_off) : t->a, cs ? (uint64_t)cfg->m_tiles * 128 : M,
+                      cs ? N : K, 64, 128);
+  if (conv2)  // GEMM1 operand: the scratch as an NHWC map [batch][h][w][oc1], im2col boxes of the k2 x k2 window
+    ok = ok && make_map_im2col(&mC, wsb + wl.c_off, (int)N, conv->w, conv->h, conv->batch, conv->k2);
+  else
+    mC = mCs;
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   cudaLaunchConfig_t lc = {};
@@ -326,18 +335,20 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.prof = g_prof;
   a.dbg = g_dbg;
   a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
-  if (implicit) {
-    a.conv_k1 = conv->k1;
+  if (implicit || conv2) {
+    a.conv_k1 = implicit ? conv->k1 : 0;
     a.conv_H = conv->h;
     a.conv_W = conv->w;
     a.conv_cblk = conv->ic / 64;
+    a.conv2_k = conv2 ? conv->k2 : 0;
+    a.conv2_cblk = (int)(N / 64);
   }
 
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, a);
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
   return FF_OK;
@@ -760,7 +771,7 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   ffKernelConfig cfg = *cfg_in;
   rc = finish_config(ch, &cfg, num_sms_cached());
   if (rc) return rc;
-  const size_t need = ws_layout(ch, &cfg).total;
+  const size_t need = ws_layout(ch, &cfg, conv != nullptr && conv->k2 > 1).total;
   if (need && (ws == nullptr || ws_bytes < need)) return fail(FF_ERR_ARG, "workspace too small");
   // L2 ready flags live in the lower half of the flag region (the pair
   // kernel's split slab flags use the upper half)
@@ -789,8 +800,14 @@ int ff_conv_chain_desc(const ffConvDesc* cv, ffChainDesc* out) {
   if (!cv || !out) return fail(FF_ERR_ARG, "null conv descriptor or output");
   if (cv->batch < 1 || cv->h < 1 || cv->w < 1 || cv->ic < 1 || cv->oc1 < 1 || cv->oc2 < 1 || cv->k1 < 1 || cv->k2 < 1)
     return fail(FF_ERR_ARG, "conv extents must be positive");
-  if (cv->k2 != 1) return fail(FF_ERR_UNSUPPORTED, "only a pointwise (1x1) second convolution is supported");
-  if (cv->k1 % 2 == 0) return fail(FF_ERR_UNSUPPORTED, "same padding needs an odd filter size");
+  if (cv->k2 != 1 && cv->k1 != 1)
+    return fail(FF_ERR_UNSUPPORTED, "one of the two convolutions must be pointwise (1x1)");
+  if (cv->k1 % 2 == 0 || cv->k2 % 2 == 0) return fail(FF_ERR_UNSUPPORTED, "same padding needs an odd filter size");
+  if (cv->k2 > 1 && (cv->oc1 % 64 || cv->oc1 > 128 || (cv->oc2 != 64 && cv->oc2 != 128 && cv->oc2 != 256)))
+    return fail(FF_ERR_UNSUPPORTED,
+                "k2 x k2 second conv: oc1 in {64, 128} (whole intermediate per CTA), oc2 in {64, 128, 256}");
+  if (cv->k2 > 1 && (cv->k2 / 2 > 127 || cv->h > 65535 || cv->w > 65535))
+    return fail(FF_ERR_UNSUPPORTED, "filter / feature map outside the im2col TMA ranges");
   if (cv->k1 > 1 && cv->ic % 64)
     return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv needs input channels in multiples of 64");
   if (cv->k1 > 1 && (cv->k1 / 2 > 127 || cv->h > 65535 || cv->w > 65535))
@@ -813,13 +830,34 @@ int ff_conv_chain_lower(const ffConvDesc* cv, int32_t num_sms, int32_t exchange,
   if (rc) return rc;
   if (cv->k1 > 1 && exchange == FF_XCHG_L2_PAIR)
     return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv runs on the 1-CTA kernels (dsm / l2 exchange)");
+  if (cv->k2 > 1) {
+    // 1x1 conv -> act -> k2 x k2 conv: every CTA computes the whole intermediate
+    // (all oc1 channels) of its 128-pixel tile, publishes it through the L2
+    // scratch, and GEMM1 reads im2col boxes of it once its neighbour tiles
+    // (the k2 x k2 halo rows) are published too
+    if (exchange != FF_XCHG_L2) return fail(FF_ERR_UNSUPPORTED, "k2 x k2 second conv runs on the l2 exchange");
+    if (!out) return fail(FF_ERR_ARG, "null output");
+    ffKernelConfig c = {};
+    c.exchange = FF_XCHG_L2;
+    c.ring = 1;
+    c.n_splits = 1;
+    c.nb = cv->oc1;
+    c.lb = cv->oc2;
+    rc = finish_config(&ch, &c, num_sms <= 0 ? 148 : num_sms);
+    if (rc) return rc;
+    if (c.units > c.rings) return fail(FF_ERR_UNSUPPORTED, "feature map needs more 128-pixel tiles than SMs");
+    *out = c;
+    return FF_OK;
+  }
   return ff_auto_config_ex(&ch, num_sms, exchange, out);
 }
 
-size_t ff_conv_chain_workspace_bytes(const ffConvDesc* cv, const ffKernelConfig* cfg) {
+size_t ff_conv_chain_workspace_bytes(const ffConvDesc* cv, const ffKernelConfig* cfg_in) {
   ffChainDesc ch;
-  if (ff_conv_chain_desc(cv, &ch)) return 0;
-  return ff_chain_workspace_bytes(&ch, cfg);
+  if (ff_conv_chain_desc(cv, &ch) || !cfg_in) return 0;
+  ffKernelConfig cfg = *cfg_in;
+  if (finish_config(&ch, &cfg, 148)) return 0;
+  return ws_layout(&ch, &cfg, cv->k2 > 1).total;
 }
 
 int ff_conv_chain_launch(const ffConvDesc* cv, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
@@ -829,6 +867,15 @@ int ff_conv_chain_launch(const ffConvDesc* cv, const ffKernelConfig* cfg, const 
   if (rc) return rc;
   if (cfg && cv->k1 > 1 && cfg->exchange == FF_XCHG_L2_PAIR)
     return fail(FF_ERR_UNSUPPORTED, "implicit-GEMM conv runs on the 1-CTA kernels (dsm / l2 exchange)");
+  if (cfg && cv->k2 > 1 &&
+      (cfg->exchange != FF_XCHG_L2 || cfg->ring != 1 || cfg->n_splits != 1 || cfg->nb != cv->oc1 || cfg->lb != cv->oc2))
+    return fail(FF_ERR_UNSUPPORTED, "k2 x k2 second conv needs the configuration of ff_conv_chain_lower");
+  if (cfg && cv->k2 > 1) {  // every tile's CTA co-resident: the halo waits must not block an unscheduled tile
+    ffKernelConfig c2 = *cfg;
+    int rc2 = finish_config(&ch, &c2, num_sms_cached());
+    if (rc2) return rc2;
+    if (c2.units > c2.rings) return fail(FF_ERR_UNSUPPORTED, "feature map needs more 128-pixel tiles than SMs");
+  }
   return launch_common(&ch, cfg, t, ws, ws_bytes, nullptr, stream, cv);
 }
 

@@ -77,6 +77,11 @@ struct ChainArgs {
   int conv_k1;         // filter size of the first convolution (0: plain A[M][K])
   int conv_H, conv_W;  // feature map height / width (M = batch * H * W output pixels)
   int conv_cblk;       // input channels / 64
+  // 1x1 conv -> act -> conv2_k x conv2_k conv (conv2_k > 1; ring 1, one n-step):
+  // C goes to the L2 scratch (NHWC) and GEMM1 k-block kb2 = (tap, 64-channel
+  // block of C) reads an im2col box of it once the halo tiles are published
+  int conv2_k;
+  int conv2_cblk;      // oc1 / 64
   uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits
   unsigned long long* prof;  // optional diagnostics: per CTA [FF_PROF_STRIDE] = 16 wait-cycle counters + 16 globaltimer stamps
 };
@@ -240,7 +245,8 @@ template <bool kGated, int kNB, int kLB, int kStages, int kMode>
 __global__ void __launch_bounds__(256, 1)
     ff_chain_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
-                    const __grid_constant__ CUtensorMap tmC, const ChainArgs args) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCs,
+                    const ChainArgs args) {
   using C = ChainCfg<kGated, kNB, kLB, kStages, kMode>;
   constexpr bool kDSM = (kMode == XCHG_DSM);
   extern __shared__ uint8_t smem_raw[];
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int h = 0; h < 16; ++h) *reinterpret_cast<volatile uint32_t*>(smem_gen + (counter(h) - base)) = 0u;
     mbar_init(own_full, 128);
     // own slot reusable after: MMA hop 0 commit + (DSM: all pushes acked | L2: TMA store done)
-    mbar_init(own_free, G == 1 ? 1 : 2);
+    mbar_init(own_free, (G == 1 && args.conv2_k <= 1) ? 1 : 2);
     mbar_init(e_full, 1);
     mbar_init(e_empty, 128);
     fence_mbar_init();
@@ -316,7 +322,10 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tmB0);
     if (kGated) tma_prefetch_desc(&tmB1);
     tma_prefetch_desc(&tmD);
-    if (!kDSM && G > 1) tma_prefetch_desc(&tmC);
+    if (!kDSM && (G > 1 || args.conv2_k > 1)) {
+      tma_prefetch_desc(&tmC);
+      tma_prefetch_desc(&tmCs);
+    }
   }
   if (warp == 1) tmem_alloc<C::kTMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -377,6 +386,34 @@ __global__ void __launch_bounds__(256, 1)
       auto load_hop = [&](int T, int h) {
         const Unit u = unit_of(T / steps);
         const int t = T % steps;
+        if (args.conv2_k > 1) {
+          // wait for every 128-pixel tile the k2 x k2 window of this tile reaches
+          const int pad = args.conv2_k / 2, W = args.conv_W;
+          const int lo = max(0, u.m0 - pad * W - pad), hi = min(args.M - 1, u.m0 + C::BM - 1 + pad * W + pad);
+          for (int tile = lo / C::BM; tile <= hi / C::BM; ++tile) {
+            const uint32_t* f = args.flags + tile;  // unit id == m tile (ring 1, one step, one l cluster)
+            uint32_t polls = 0;
+            FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+              if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+            });
+          }
+          fence_proxy_async_global();
+          const int hw = args.conv_H * W, img = u.m0 / hw, rem = u.m0 % hw;
+          const int nk = args.conv2_k * args.conv2_k * args.conv2_cblk;
+          for (int kb2 = 0; kb2 < nk; ++kb2) {
+            const int tap = kb2 / args.conv2_cblk, cb = kb2 % args.conv2_cblk;
+            FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
+            const uint32_t sb = base + stage * C::kSTAGE;
+            mbar_expect_tx(full_bar(stage), C::kG1_BYTES);
+            tma_load_im2col_4d(sb, &tmC, full_bar(stage), cb * 64, rem % W - pad, rem / W - pad, img,
+                               (uint16_t)(tap % args.conv2_k), (uint16_t)(tap / args.conv2_k));
+#pragma unroll
+            for (int j = 0; j < kLB / 64; ++j)
+              tma_load_2d(sb + C::kG1_DOFF + j * 8192, &tmD, full_bar(stage), u.l0 + 64 * j, kb2 * C::BK);
+            next();
+          }
+          return;
+        }
         const int origin = ((int)p - h + G) % G;
         const int nrow0 = u.n0 + (t * G + origin) * kNB;
         const bool remote_c = !kDSM && h > 0;
@@ -482,8 +519,9 @@ __global__ void __launch_bounds__(256, 1)
           slot = recv_slot[b];
         }
         tc_fence_after();
-        const bool from_stage = !kDSM && h > 0;
-        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+        const bool from_stage = (!kDSM && h > 0) || args.conv2_k > 1;
+        const int nk = args.conv2_k > 1 ? args.conv2_k * args.conv2_k * args.conv2_cblk : C::kCW / C::BK;
+        for (int kb2 = 0; kb2 < nk; ++kb2) {
           FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
@@ -612,14 +650,14 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive(c_empty[cb]);
       fence_proxy_async_smem();
       mbar_arrive(own_full);
-      if (!kDSM && G > 1) {
+      if (!kDSM && (G > 1 || args.conv2_k > 1)) {
         // publish the chunk through L2: TMA store, then release the ready flag
         named_bar_sync(1, 128);
         if (warp == 4 && lane_id() == 0) {
           const int ncol = u.n0 + (t * G + (int)p) * kNB;
 #pragma unroll
           for (int sub = 0; sub < C::kCW / 64; ++sub)
-            tma_store_2d(&tmC, own_slot + sub * (C::BM * C::BK * 2), ncol + 64 * sub, u.m0);
+            tma_store_2d(&tmCs, own_slot + sub * (C::BM * C::BK * 2), ncol + 64 * sub, u.m0);
           bulk_commit();
           bulk_wait0();
           fence_proxy_async_global();

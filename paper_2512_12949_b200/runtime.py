@@ -14,7 +14,7 @@ from typing import Optional
 
 from . import _native as nat
 from .plan import FusionPlan
-from .workload import DIMS, GATED_FFN, ChainGraph, ConvChainConfig
+from .workload import DIMS, GATED_FFN, ChainGraph, ConvBlockConfig, ConvChainConfig
 
 _workspaces: dict = {}
 
@@ -204,11 +204,12 @@ def profile_configs(graph: ChainGraph, cfgs, tensors: dict, iters: int = 10, war
 # ----------------------------------------------------------------------------- conv chains
 
 
-def conv_desc(cfg: ConvChainConfig, batch: int = 1, activation: str = "relu") -> nat.ConvDesc:
+def conv_desc(cfg, batch: int = 1, activation: str = "relu") -> nat.ConvDesc:
+    """ffConvDesc of a ConvChainConfig (reference) or ConvBlockConfig (k2 > 1 extension)."""
     return nat.ConvDesc(batch, cfg.h, cfg.w, cfg.ic, cfg.oc1, cfg.oc2, cfg.k1, cfg.k2, nat.ACT[activation])
 
 
-def lower_conv(cfg: ConvChainConfig, batch: int = 1, exchange: str = "auto", activation: str = "relu",
+def lower_conv(cfg, batch: int = 1, exchange: str = "auto", activation: str = "relu",
                num_sms: Optional[int] = None) -> nat.KernelConfig:
     """Physical launch for a conv chain (ConvChainConfig, workload.py:168-184).
     k1 > 1 runs as an implicit GEMM on the 1-CTA kernels ("dsm" / "l2")."""
@@ -226,18 +227,20 @@ def lower_conv(cfg: ConvChainConfig, batch: int = 1, exchange: str = "auto", act
     raise last
 
 
-def launch_conv(cfg: ConvChainConfig, kcfg: nat.KernelConfig, x, w1, w2, out=None, stream=None,
-                activation: str = "relu"):
-    """conv(k1 x k1, same padding) -> act -> conv(1 x 1) on NHWC bf16 tensors:
-    x [batch, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2]; returns
-    y [batch, h, w, oc2].  GEMM0 reads x through an im2col tensor map."""
+def launch_conv(cfg, kcfg: nat.KernelConfig, x, w1, w2, out=None, stream=None, activation: str = "relu"):
+    """conv(k1 x k1, same padding) -> act -> conv(k2 x k2) on NHWC bf16 tensors:
+    x [batch, h, w, ic], w1 [k1, k1, ic, oc1] (HWIO), w2 [oc1, oc2] (k2 == 1) or
+    [k2, k2, oc1, oc2]; returns y [batch, h, w, oc2].  k1 > 1: GEMM0 reads x
+    through an im2col tensor map; k2 > 1 (ConvBlockConfig): GEMM1 reads the
+    L2-resident intermediate through one."""
     import torch
 
     lib = nat.load()
     if not torch.cuda.is_available():
         raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
     batch = x.shape[0]
-    shapes = {"x": (batch, cfg.h, cfg.w, cfg.ic), "w1": (cfg.k1, cfg.k1, cfg.ic, cfg.oc1), "w2": (cfg.oc1, cfg.oc2)}
+    w2_shape = (cfg.oc1, cfg.oc2) if cfg.k2 == 1 else (cfg.k2, cfg.k2, cfg.oc1, cfg.oc2)
+    shapes = {"x": (batch, cfg.h, cfg.w, cfg.ic), "w1": (cfg.k1, cfg.k1, cfg.ic, cfg.oc1), "w2": w2_shape}
     for name, t in (("x", x), ("w1", w1), ("w2", w2)):
         if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
@@ -253,7 +256,7 @@ def launch_conv(cfg: ConvChainConfig, kcfg: nat.KernelConfig, x, w1, w2, out=Non
     return out
 
 
-def run_conv(cfg: ConvChainConfig, x, w1, w2, out=None, stream=None, exchange: str = "auto",
+def run_conv(cfg, x, w1, w2, out=None, stream=None, exchange: str = "auto",
              activation: str = "relu"):
     """Execute a conv chain on the current GPU (the reference's conv presets
     C1-C8, workload.py:207-240, without materialising the im2col matrix)."""

@@ -27,12 +27,51 @@ GPU_CASES = [
 ]
 
 
-def _conv_inputs(ic, h, w, oc1, oc2, k1, batch, seed=0):
+def _conv_inputs(ic, h, w, oc1, oc2, k1, batch, seed=0, k2=1):
     rng = np.random.default_rng(seed)
     x = oracle.round_bf16(rng.uniform(-1, 1, (batch, h, w, ic)).astype(np.float32))
     w1 = oracle.round_bf16((rng.uniform(-1, 1, (k1, k1, ic, oc1)) / np.sqrt(k1 * k1 * ic)).astype(np.float32))
-    w2 = oracle.round_bf16((rng.uniform(-1, 1, (oc1, oc2)) / np.sqrt(oc1)).astype(np.float32))
+    w2_shape = (oc1, oc2) if k2 == 1 else (k2, k2, oc1, oc2)
+    w2 = oracle.round_bf16((rng.uniform(-1, 1, w2_shape) / np.sqrt(k2 * k2 * oc1)).astype(np.float32))
     return x, w1, w2
+
+
+# extension: 1x1 conv -> ReLU -> k2 x k2 conv (ResNet bottleneck order, BASELINE.json configs[3])
+BLOCK_CASES = [
+    ("resnet-c2x-56", (256, 56, 56, 64, 64, 1, 3), 1),
+    ("resnet-c3x-28", (512, 28, 28, 128, 128, 1, 3), 1),
+    ("b2-5x5-ragged", (128, 9, 11, 64, 256, 1, 5), 2),
+    ("b1-3x3-tiny", (64, 5, 6, 128, 64, 1, 3), 1),
+]
+
+
+@pytest.mark.parametrize("k2", [3, 5])
+def test_block_oracle_matches_direct_conv(k2):
+    torch = pytest.importorskip("torch")
+    x, w1, w2 = _conv_inputs(16, 7, 9, 24, 8, 1, 2, seed=k2, k2=k2)
+    got = oracle.conv_chain(x, w1, w2, "relu")
+    xt = torch.from_numpy(x).permute(0, 3, 1, 2).double()
+    c = torch.nn.functional.conv2d(xt, torch.from_numpy(w1).permute(3, 2, 0, 1).double()).relu()
+    y = torch.nn.functional.conv2d(c, torch.from_numpy(w2).permute(3, 2, 0, 1).double(), padding=k2 // 2)
+    assert oracle.max_relative_error(got, y.permute(0, 2, 3, 1).numpy()) < 1e-5
+
+
+def test_block_config_rules():
+    from paper_2512_12949_b200 import runtime, workload as W
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200.errors import UnsupportedConvChain
+
+    with pytest.raises(UnsupportedConvChain):  # the reference's class keeps its k2 == 1 rule
+        W.ConvChainConfig(64, 8, 8, 64, 64, 1, 3)
+    with pytest.raises(UnsupportedConvChain):
+        W.ConvBlockConfig(64, 8, 8, 64, 64, 3, 3)
+    cfg = runtime.lower_conv(W.ConvBlockConfig(256, 56, 56, 64, 64, 1, 3), exchange="l2")
+    assert (cfg.ring, cfg.n_splits, cfg.nb, cfg.lb, cfg.units) == (1, 1, 64, 64, 25)
+    for exchange in ("dsm", "pair"):
+        with pytest.raises(nat.UnsupportedPlan):
+            runtime.lower_conv(W.ConvBlockConfig(256, 56, 56, 64, 64, 1, 3), exchange=exchange)
+    with pytest.raises(nat.UnsupportedPlan):  # the whole intermediate of a tile: oc1 <= 128
+        runtime.lower_conv(W.ConvBlockConfig(256, 14, 14, 256, 64, 1, 3), exchange="l2")
 
 
 @pytest.mark.parametrize("k1", [1, 3, 5])
@@ -95,3 +134,30 @@ def test_conv_chain_matches_oracle(case, exchange):
         assert np.isfinite(got).all()
         err_b, err = oracle.max_relative_error(got, ref_b), oracle.max_relative_error(got, ref)
         assert err_b <= TOL and err <= TOL, (name, exchange, kcfg.as_dict(), err_b, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", BLOCK_CASES, ids=lambda c: c[0])
+def test_conv_block_matches_oracle(case):
+    """1x1 -> ReLU -> k2 x k2: GEMM1 reads im2col boxes of the L2-resident
+    intermediate after the halo tiles are published (parity unpinned: no
+    reference counterpart; the oracle is pinned to torch's direct conv above)."""
+    import torch
+
+    from paper_2512_12949_b200 import runtime, workload as W
+
+    name, shape, batch = case
+    cfg = W.ConvBlockConfig(*shape)
+    ic, h, w, oc1, oc2, k1, k2 = shape
+    x, w1, w2 = _conv_inputs(ic, h, w, oc1, oc2, k1, batch, seed=3, k2=k2)
+    dev = [torch.from_numpy(a).cuda().to(torch.bfloat16).contiguous() for a in (x, w1, w2)]
+    kcfg = runtime.lower_conv(cfg, batch, "l2")
+    for _ in range(2):
+        y = runtime.launch_conv(cfg, kcfg, *dev)
+        torch.cuda.synchronize()
+        got = y.float().cpu().numpy()
+        ref_b = oracle.conv_chain(x, w1, w2, "relu", bf16_intermediate=True)
+        ref = oracle.conv_chain(x, w1, w2, "relu")
+        err_b, err = oracle.max_relative_error(got, ref_b), oracle.max_relative_error(got, ref)
+        assert np.isfinite(got).all()
+        assert err_b <= TOL and err <= TOL, (name, kcfg.as_dict(), err_b, err)
