@@ -283,6 +283,15 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     ok = ok && make_map_im2col(&mC, wsb + wl.c_off, (int)N, conv->w, conv->h, conv->batch, conv->k2);
   else
     mC = mCs;
+  CUtensorMap mE, mW;  // E tile outputs: bf16 E [M][L] box {64, 128}; fp32 split-N workspace [M][L] box {32, 128}
+  {
+    const uint64_t de[2] = {L, M}, se[1] = {L * 2};
+    const uint32_t be[2] = {64, 128};
+    ok = ok && make_map_nd(&mE, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, t->e, de, se, be);
+    const uint64_t sw[1] = {L * 4};
+    const uint32_t bw[2] = {32, 128};
+    ok = ok && make_map_nd(&mW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, wsb + wl.e_off, de, sw, bw);
+  }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   cudaLaunchConfig_t lc = {};
@@ -348,7 +357,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, a);
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, mE, mW, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
   return FF_OK;

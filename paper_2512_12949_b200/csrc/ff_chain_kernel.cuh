@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(256, 1)
     ff_chain_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCs,
+                    const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmW,
                     const ChainArgs args) {
   using C = ChainCfg<kGated, kNB, kLB, kStages, kMode>;
   constexpr bool kDSM = (kMode == XCHG_DSM);
@@ -670,34 +671,67 @@ __global__ void __launch_bounds__(256, 1)
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait(e_full, (T / steps) & 1);
         tc_fence_after();
-        const int grow = u.m0 + row;
+        // E tile through the own slot (free once hop 0, the pushes / the C store are done)
+        // in SW128 16 KB tiles, leaving by bulk tensor ops: bf16 TMA stores (S == 1) or
+        // fp32 TMA reduce-adds into the split-N workspace (per-thread rows would be 32
+        // scattered lines per warp access; measured ~16 GB/s per SM with red.global.add)
+        mbar_wait(own_free, T & 1);
+        const bool f32 = args.S > 1;
+        const int cpt = f32 ? 32 : 64;  // columns per 16 KB tile
+        // the ring's final unit stages the whole tile at once in the drained pipeline
+        // stages (no load follows); earlier units use the own slot in rounds
+        const bool final_unit = (T / steps) == my_units - 1;
+        const uint32_t stg = final_unit ? base : own_slot;
+        const int tpr = final_unit ? (C::kOFF_OWN / 16384) : (C::kCHUNK_BYTES / 16384);  // tiles per round
+        const bool issuer = (warp == 4 && lane_id() == 0);
 #pragma unroll 1
-        for (int c0 = 0; c0 < kLB; c0 += 16) {
-          float v[16];
-          tmem_ld16(lane_base + C::kTMEM_E + c0, v);
-          if (grow < args.M) {
-            if (args.S == 1) {
+        for (int g0 = 0; g0 < kLB; g0 += cpt * tpr) {
+          const int g1 = min(kLB, g0 + cpt * tpr);
+#pragma unroll 1
+          for (int c0 = g0; c0 < g1; c0 += 16) {
+            float v[16];
+            tmem_ld16(lane_base + C::kTMEM_E + c0, v);
+            const uint32_t rowb = stg + ((c0 - g0) / cpt) * 16384 + row * 128;
+            if (f32) {
+              const int j0 = (c0 % 32) / 4;
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                st_shared_v4(rowb + (((j0 + j) ^ (row & 7)) << 4), __float_as_uint(v[4 * j]),
+                             __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                             __float_as_uint(v[4 * j + 3]));
+            } else {
               uint32_t pk[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-              uint4* dst = reinterpret_cast<uint4*>(args.E + (size_t)grow * args.L + u.l0 + c0);
-              dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-            } else {
-              float* dst = args.ws + (size_t)grow * args.L + u.l0 + c0;
-#pragma unroll
-              for (int i = 0; i < 16; i += 4) red_add_v4_f32(dst + i, v[i], v[i + 1], v[i + 2], v[i + 3]);
+              const int j0 = (c0 % 64) / 8;
+              st_shared_v4(rowb + ((j0 ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
+              st_shared_v4(rowb + (((j0 + 1) ^ (row & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
             }
           }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (issuer) {
+            for (int c = g0; c < g1; c += cpt) {
+              const uint32_t tile = stg + ((c - g0) / cpt) * 16384;
+              if (f32)
+                tma_reduce_add_2d(&tmW, tile, u.l0 + c, u.m0);
+              else
+                tma_store_2d(&tmE, tile, u.l0 + c, u.m0);
+            }
+            bulk_commit();
+            bulk_wait_read0_group();
+          }
+          named_bar_sync(1, 128);
         }
         tc_fence_before();
         mbar_arrive(e_empty);
         if (args.S > 1)
           split_finish<kLB>(args, args.tile_cnt + (u.m0 / C::BM) * (args.L / kLB) + u.l0 / kLB, tmem_slot + 8,
-                            warp == 4 && lane_id() == 0, false, u.m0, row, u.l0, 1, args.n_units <= args.n_rings);
+                            issuer, true, u.m0, row, u.l0, 1, args.n_units <= args.n_rings);
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
+    if (warp == 4 && lane_id() == 0) bulk_wait0();  // E stores / reduce-adds performed before exit
     if (args.prof && warp == 4 && lane_id() == 0) {
       unsigned long long* pr = args.prof + blockIdx.x * FF_PROF_STRIDE;
       pr[9] = clock64() - t_start;
