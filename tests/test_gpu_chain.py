@@ -226,3 +226,31 @@ def test_split_reduction_leaves_workspace_zero(exchange, ring, splits, nb, lb):
     ws = runtime._workspaces[(torch.cuda.current_device(), int(stream.cuda_stream))]
     lo, hi = 1 << 20, (1 << 20) + (256 << 10) + m * l * 4
     assert int(ws[lo:hi].count_nonzero()) == 0
+
+
+# pair-kernel variants behind debug bits (ff_set_debug_mode): helper pairs on the idle
+# SMs (bit 26, opt-in), common GEMM0 k order (bit 27), plain pair kernel (bit 6)
+@pytest.mark.parametrize("mode", [1 << 26, 1 << 27, 64], ids=["helpers", "no-krot", "no-quad"])
+@pytest.mark.parametrize("case", [("gated_ffn", "silu", 512, 8192, 2048, 2048),
+                                  ("standard_ffn", "relu", 512, 16384, 4096, 4096)], ids=["llama1b", "gpt67b"])
+def test_pair_kernel_variants_match_oracle_and_repeat_bitwise(case, mode):
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    host, dev = _inputs(kind, m, n, k, l, seed=11)
+    lib = nat.load()
+    lib.ff_set_debug_mode(mode)
+    try:
+        cfg = runtime.lower(graph, None, 148, "pair")
+        if mode == 1 << 26:
+            assert cfg.helpers > 0 and cfg.helper_x > 0
+        out1 = runtime.launch(graph, cfg, dev).clone()
+        out2 = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+    finally:
+        lib.ff_set_debug_mode(0)
+    _check(kind, act, host, out1)
+    assert torch.equal(out1, out2), "split-N / helper reductions must be deterministic"

@@ -49,13 +49,13 @@ def test_library_exports_every_declared_symbol(lib):
 def test_struct_layouts_match_the_header(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include "ff_chain.h"\n'
-                   'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(ffChainDesc), sizeof(ffPlanDesc),'
-                   ' sizeof(ffKernelConfig), sizeof(ffTensors));return 0;}\n')
+                   'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(ffChainDesc), sizeof(ffPlanDesc),'
+                   ' sizeof(ffKernelConfig), sizeof(ffTensors), sizeof(ffConvDesc));return 0;}\n')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", INC, str(src), "-o", str(exe)], check=True)
     sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     assert sizes == [ctypes.sizeof(nat.ChainDesc), ctypes.sizeof(nat.PlanDesc), ctypes.sizeof(nat.KernelConfig),
-                     ctypes.sizeof(nat.Tensors)]
+                     ctypes.sizeof(nat.Tensors), ctypes.sizeof(nat.ConvDesc)]
 
 
 def _check_cfg(graph, cfg):
