@@ -313,6 +313,15 @@ def time_steps(fn, steps, flush, stream):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def _max_over_ranks(x, dev):
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -357,9 +366,7 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     total_ms = float(sum(times))
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = _max_over_ranks(total_ms, dev)
     fl = flops_of(kind, m, n, k, l)
     value = fl * args.steps * world / (total_ms * 1e-3) / 1e12
     ms_step = total_ms / args.steps
@@ -382,9 +389,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_times = time_steps(e2e_step, args.steps, flush, stream)
     e2e_ms = float(sum(e2e_times))
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = _max_over_ranks(e2e_ms, dev)
     e2e_value = fl * args.steps * world / (e2e_ms * 1e-3) / 1e12
 
     # unfused cuBLAS on the same config
@@ -475,6 +480,14 @@ def run_reference(args, rank, world):
         return None
     kind, act, m, n, k, l, desc = WORKLOADS[args.workload]
     import oracle
+
+    # all host threads for the BLAS (torchrun exports OMP_NUM_THREADS=1 to every rank)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(limits=len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
 
     # each step = one plan-faithful replay of a token-row sample of the chain,
     # sized so the whole --steps K --warmup W run stays within ~2 minutes
@@ -649,8 +662,13 @@ def main():
     if world > 1:
         import torch
 
+        # one process per GPU over NCCL (host-side barrier + max-over-ranks only: the chain
+        # shards on tokens with no data-path collective).  With fewer GPUs than ranks
+        # (validating the N-rank path on a 1-GPU box) ranks share devices and use gloo.
+        shared = torch.cuda.device_count() < world
+        local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if shared else "nccl")
     doc = run_ours(args, rank, world, local_rank)
     if doc is not None:
         if not args.no_cpu and world == 1:
