@@ -13,7 +13,7 @@ stamps = torch.zeros(64, dtype=torch.int64, device='cuda')
 stream = torch.cuda.current_stream().cuda_stream
 def stamp(i):
     assert lib.ff_stamp_globaltimer(ctypes.c_void_p(stamps.data_ptr() + 8 * i), ctypes.c_void_p(stream)) == 0
-NFLUSH = 4 if 'deep' in ARGV else 1
+NFLUSH = 4 if 'deep' in ARGV else (0 if 'warm' in ARGV else 1)
 SHAPES = {"llama": (512,8192,2048,2048,2,True), "gpt67b": (512,16384,4096,4096,1,False),
           "gpt2s": (512,3072,768,768,3,False), "opt": (4096,8192,2048,2048,1,False)}
 for name, shape in ([] if 'probe' in ARGV else SHAPES.items() if 'opt' in ARGV else list(SHAPES.items())[:3]):
