@@ -865,8 +865,10 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
-      if (slice != sp) __threadfence();
     }
+    // the barrier orders every thread's region stores before the issuer's
+    // gpu-scope release (cumulative; the split-K semaphore pattern), no
+    // per-thread fence
     __syncthreads();
     if (issuer) {
       FF_STAMP(24);
