@@ -733,6 +733,13 @@ int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, 
   }
   c.n_splits = 1;
   fill_machine(ch, &c, num_sms);
+  // A chain too small to occupy half the SMs with rings of one CTA (a latency-bound
+  // conv tile row): narrower E slices, i.e. more l clusters that each recompute
+  // their cheap GEMM0 (conv C5: 25 -> 100 CTAs, 15.3 -> 13.3 us, profiles/r01/conv_sweep.log)
+  if (exchange != FF_XCHG_L2_PAIR && c.ring == 1) {
+    const int64_t m_tiles = (ch->m + 127) / 128;
+    while (c.lb > 64 && m_tiles * (ch->l / c.lb) * c.n_splits < num_sms / 2) c.lb /= 2;
+  }
   rc = finish_config(ch, &c, num_sms);
   if (rc) return rc;
   *out = c;
