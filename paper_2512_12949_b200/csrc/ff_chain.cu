@@ -163,7 +163,7 @@ int table_active_clusters(int cluster, int num_sms) {
 }
 
 struct WsLayout {
-  size_t e_off, c_off, f_off, n_off, s_off, total;
+  size_t e_off, c_off, f_off, n_off, s_off, h_off, total;
   bool e_memset;  // fp32 E larger than the zero zone: clear it before the launch
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -191,14 +191,19 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   w.n_off = kFlagBytes;
   w.e_off = kFlagBytes + kCntBytes;
   w.e_memset = e_bytes > kEZoneBytes;
-  size_t off = w.e_off + e_bytes;
-  if (c_scratch) off = w.e_off + std::max(e_bytes, kEZoneBytes);
+  // everything after the fp32 E zone starts past its full 32 MiB: regions of one
+  // config must never overlap the zero-invariant zone another config relies on
+  // (a gated ring-1 split config once put its exchange regions there)
+  size_t off = w.e_off + std::max(e_bytes, kEZoneBytes);
   w.c_off = off;
   if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
   w.s_off = off;
   if (pair && c->n_splits > 1)
     off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * 256 * ch->l * sizeof(float));
+  // helper pairs' E partials, one region per (E tile, n-step); plain stores, no zero invariant
+  w.h_off = off;
+  if (pair && c->helpers > 0) off = align256(off + (size_t)c->steps * c->m_tiles * 256 * ch->l * sizeof(float));
   w.total = off;
   return w;
 }
@@ -232,7 +237,6 @@ void plan_helpers(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   if (!pair_finish_regions(ch, c, c->rings) || c->steps > 2 || c->l_clusters != 1) return;
   const int H = (num_sms - c->rings * c->ring * 2) / 2;
   if (H < 1) return;
-  if ((size_t)c->steps * c->m_tiles * 256 * ch->l * sizeof(float) > kEZoneBytes) return;  // helper regions
   const double r = (double)ch->k / (ch->kind == FF_KIND_GATED ? 128 : 256);
   const double G = c->ring, st = c->steps, units = c->units;
   // members: st*r + st*(G - x) hop-times; helpers: r + 2 (first chunks drained and
@@ -487,9 +491,6 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const uint64_t ds[3] = {32, 16, tiles * S * 64}, ss[2] = {128, 2048};
     const uint32_t bs[3] = {32, rs / 8, 64};
     ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sp, ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
-    const uint64_t dz[3] = {32, 16, tiles * 64};
-    ok = ok && make_map_nd(&maps.hz, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, wsb + wl.e_off, dz, ss, bs,
-                           CU_TENSOR_MAP_SWIZZLE_NONE);
   }
     if (ok) {
       cache[cache_next].key = key;
@@ -537,7 +538,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // helper pairs (planned by finish_config for the non-quad launch)
   a.helpers = (!kQuad && rings == cfg->rings) ? cfg->helpers : 0;
   a.helper_x = a.helpers > 0 ? cfg->helper_x : 0;
-  a.hzone = reinterpret_cast<float*>(wsb + wl.e_off);
+  a.hzone = reinterpret_cast<float*>(wsb + wl.h_off);
   if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);
   a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
   // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
@@ -721,16 +722,27 @@ int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, 
   c.exchange = exchange;
   const bool gated = ch->kind == FF_KIND_GATED;
   const int max_ring = exchange == FF_XCHG_DSM ? 16 : (exchange == FF_XCHG_L2_PAIR ? num_sms / 2 : num_sms);
-  c.lb = pick_lb(ch->l, max_ring);
-  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "l cannot be covered by one ring");
-  c.ring = (int32_t)(ch->l / c.lb);
-  if (exchange == FF_XCHG_L2_PAIR) {
-    if (c.lb < 128) return fail(FF_ERR_UNSUPPORTED, "pair kernel needs l slices of >= 128 columns");
-    c.nb = gated ? 128 : 256;
-  } else {
-    c.nb = gated ? 64 : 128;
-    if (ch->n % ((int64_t)c.ring * c.nb)) c.nb = 64;
+  // E slice width lb (widest first), then the largest ring of lb slices whose
+  // n-step (ring * nb C columns) divides N; l slices the ring does not cover
+  // become l clusters (each recomputes GEMM0 for its part of L)
+  const bool pair = exchange == FF_XCHG_L2_PAIR;
+  const int nb_opts[2] = {pair ? (gated ? 128 : 256) : (gated ? 64 : 128), pair ? 0 : 64};
+  c.lb = 0;
+  for (int lb : {256, 128, 64}) {
+    if (c.lb || ch->l % lb || (pair && lb != 256)) continue;
+    const int64_t slices = ch->l / lb;
+    for (int64_t ring = std::min<int64_t>(slices, max_ring); ring >= 1 && !c.lb; --ring) {
+      if (slices % ring) continue;
+      for (int nb : nb_opts)
+        if (nb && ch->n % (ring * nb) == 0) {
+          c.lb = lb;
+          c.ring = (int32_t)ring;
+          c.nb = nb;
+          break;
+        }
+    }
   }
+  if (!c.lb) return fail(FF_ERR_UNSUPPORTED, "no ring of E slices whose C chunks tile n");
   c.n_splits = 1;
   fill_machine(ch, &c, num_sms);
   // A chain too small to occupy half the SMs with rings of one CTA (a latency-bound

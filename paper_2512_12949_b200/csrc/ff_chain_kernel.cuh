@@ -64,7 +64,7 @@ struct ChainArgs {
   float* slab;         // pair kernel: split-N exchange regions [E tile][split][16-B chunk][128 rows]
   int helpers;         // pair kernel: helper pairs on the SMs the rings leave idle (0 = none)
   int helper_x;        // pair kernel: last hops of every member's n-steps executed by the helpers
-  float* hzone;        // pair kernel: helper E partials, [E tile][16-B chunk][128 rows], zero between launches
+  float* hzone;        // pair kernel: helper E partials, [E tile][n-step][16-B chunk][128 rows]
   uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
   int defer;           // pair kernel: hops of step T that run after GEMM0(T+1) (< G)

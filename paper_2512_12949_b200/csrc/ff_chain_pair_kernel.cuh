@@ -37,7 +37,6 @@ struct PairMaps {
   CUtensorMap e3;   // E bf16 3D {64, M, L/64}, box {64, 128, kLB/64}
   CUtensorMap w3;   // fp32 workspace 3D {32, M, L/32}, box {32, 128, kLB/32}
   CUtensorMap er;   // E bf16 3D, box {64, 128/S, kLB/64}: one row slice of a tile
-  CUtensorMap hz;   // helper zone, same geometry as slab (S = 1)
   CUtensorMap slab; // split-N exchange regions 3D {32, 16, tiles*S*64} fp32, box {32, 128/S/8, 64} (no swizzle)
 };
 

@@ -254,3 +254,63 @@ def test_pair_kernel_variants_match_oracle_and_repeat_bitwise(case, mode):
         lib.ff_set_debug_mode(0)
     _check(kind, act, host, out1)
     assert torch.equal(out1, out2), "split-N / helper reductions must be deterministic"
+
+
+def _random_cases(n, seed):
+    rng = __import__("random").Random(seed)
+    cases = []
+    for _ in range(n):
+        kind = rng.choice(["standard_ffn", "gated_ffn"])
+        act = "silu" if kind == "gated_ffn" else rng.choice(["relu", "identity", "silu", "gelu"])
+        m = rng.choice([16, 17, 64, 128, 200, 256, 384, 640])
+        k = 128 * rng.randint(1, 12)
+        n = 256 * rng.randint(1, 16)
+        l = 256 * rng.randint(1, 8)
+        cases.append((kind, act, m, n, k, l))
+    return cases
+
+
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("case", _random_cases(10, 2025), ids=lambda c: f"{c[0][:3]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
+def test_random_shapes_match_oracle(case, exchange):
+    """Seeded random shapes (ragged M down to 16, K in 128s, N/L in 256s) under every transport."""
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    try:
+        cfg = runtime.lower(graph, None, 148, exchange)
+    except nat.UnsupportedPlan:
+        pytest.skip(f"{exchange} has no lowering for {case}")
+    host, dev = _inputs(kind, m, n, k, l, seed=3)
+    out = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    _check(kind, act, host, out)
+
+
+def test_workspace_zero_invariant_across_configs():
+    """The split counters and the fp32 E zone of the shared per-stream workspace
+    are zero after every launch (configs reuse one workspace; a config whose
+    regions overlapped the zone once corrupted the next split chain)."""
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    seq = [("gated_ffn", "silu", 128, 3328, 256, 1792), ("standard_ffn", "relu", 200, 768, 256, 768),
+           ("gated_ffn", "silu", 384, 768, 1536, 1792), ("standard_ffn", "gelu", 512, 3072, 768, 768)]
+    for case in seq:
+        for exchange in ("pair", "l2", "dsm"):
+            graph = _graph(*case)
+            try:
+                cfg = runtime.lower(graph, None, 148, exchange)
+            except nat.UnsupportedPlan:
+                continue
+            host, dev = _inputs(case[0], *case[2:], seed=5)
+            out = runtime.launch(graph, cfg, dev)
+            torch.cuda.synchronize()
+            _check(case[0], case[1], host, out)
+            for ws in runtime._workspaces.values():
+                cnt = ws[(1 << 20):(1 << 20) + (256 << 10)]
+                zone = ws[(1 << 20) + (256 << 10):(1 << 20) + (256 << 10) + (32 << 20)]
+                assert int((cnt != 0).sum()) == 0 and int((zone != 0).sum()) == 0, (case, exchange, cfg.as_dict())
