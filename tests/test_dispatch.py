@@ -1,0 +1,47 @@
+"""Run-time M-bin dispatch table: bin lookup and table
+round trip on CPU; dispatch of ragged M through the shipped tables on the GPU."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2512_12949_b200 import dispatch
+
+
+def test_shipped_tables_cover_the_baseline_families():
+    for name, (kind, act, n, k, l) in dispatch.FAMILIES.items():
+        t = dispatch.shipped(name)
+        assert (t.kind, t.activation, t.n, t.k, t.l) == (kind, act, n, k, l)
+        assert t.bins == sorted(t.bins) and len(t.configs) == len(t.bins)
+        for c in t.configs:
+            assert c["exchange"] in (0, 1, 2) and c["ring"] >= 1 and c["n_splits"] >= 1 and c["ms"] > 0
+
+
+def test_bin_lookup_and_round_trip(tmp_path):
+    t = dispatch.shipped("llama1b")
+    assert t.bin_of(1) == 0 and t.bin_of(64) == 0 and t.bin_of(65) == 1 and t.bin_of(8192) == len(t.bins) - 1
+    with pytest.raises(ValueError):
+        t.bin_of(t.bins[-1] + 1)
+    p = tmp_path / "t.json"
+    t.save(str(p))
+    u = dispatch.Dispatcher.load(str(p))
+    assert u.to_dict() == t.to_dict()
+    cfg = u.config_for(300)
+    assert (cfg.ring, cfg.n_splits, cfg.exchange) == tuple(t.configs[t.bin_of(300)][f] for f in ("ring", "n_splits",
+                                                                                                   "exchange"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,m", [("llama1b", 300), ("llama1b", 40), ("gpt2s", 777), ("opt13b", 1500)])
+def test_dispatch_ragged_m_matches_oracle(name, m):
+    import torch
+
+    t = dispatch.shipped(name)
+    kind = t.kind
+    host = {k: oracle.round_bf16(v) for k, v in oracle.make_inputs(kind, m, t.n, t.k, t.l, seed=9).items()}
+    dev = {k: torch.from_numpy(v).cuda().to(torch.bfloat16) for k, v in host.items()}
+    out = t.run(dev)
+    torch.cuda.synchronize()
+    got = out.float().cpu().numpy()
+    ref = oracle.dense_chain(kind, t.activation, host, bf16_intermediate=True)
+    assert np.isfinite(got).all() and oracle.max_relative_error(got, ref) <= 1e-2
