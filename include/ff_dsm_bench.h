@@ -40,6 +40,10 @@ int ff_stamp_globaltimer(void* dst, void* stream);
  * TMEM alloc/dealloc); CTA i writes entry/exit %globaltimer to stamps[2i], [2i+1]. */
 int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tmem, void* stream);
 
+/* Diagnostics: `ctas` one-warp CTAs spinning on clock64 for `cycles` (keeps the
+ * stream busy without touching memory, so a following launch sees a warm L2). */
+int ff_spin(long long cycles, int ctas, void* stream);
+
 const char* ff_dsm_last_error(void);
 
 #ifdef __cplusplus

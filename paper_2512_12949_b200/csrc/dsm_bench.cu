@@ -107,6 +107,12 @@ __global__ void __launch_bounds__(256, 1) launch_probe_big_kernel(const __grid_c
   }
 }
 
+__global__ void spin_kernel(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -205,6 +211,16 @@ int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tme
   } else {
     e = cudaLaunchKernelEx(&lc, launch_probe_kernel, reinterpret_cast<unsigned long long*>(stamps), tmem);
   }
+  if (e != cudaSuccess) {
+    g_err = cudaGetErrorString(e);
+    return 4;
+  }
+  return 0;
+}
+
+int ff_spin(long long cycles, int ctas, void* stream) {
+  spin_kernel<<<ctas, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(cycles);
+  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_err = cudaGetErrorString(e);
     return 4;

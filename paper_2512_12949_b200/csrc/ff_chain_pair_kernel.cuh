@@ -104,6 +104,10 @@ __global__ void __launch_bounds__(256, 1)
       vcta = 2 * (pi - min(H, (pi + 1) / stride)) + (int)q;
   }
   if (threadIdx.x == 0) FF_STAMP(16);
+  if (args.dbg & (1u << 28)) {  // diagnostics: launch latency of this binary alone
+    if (threadIdx.x == 0) FF_STAMP(31);
+    return;
+  }
   const int p = kQuad ? (vcta / 4) % G : (vcta / 2) % G;  // ring position
   const int ring = kQuad ? 2 * ((vcta / 4) / G) + (int)pq : (vcta / 2) / G;
   const uint16_t mcast = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));  // this CTA and its twin
@@ -230,7 +234,10 @@ __global__ void __launch_bounds__(256, 1)
     auto unit_at = [&](const Seg& g, int split) {  // l_clusters == 1
       return Unit{g.mt * 2 * C::BM, g.p * kLB, split * steps * G * C::kN0, g.mt + args.m_tiles * split, split};
     };
-    const uint32_t hb_full[2] = {e_full, c_full}, hb_empty[2] = {e_empty, c_empty};
+    // E buffer eb's barriers (selects, not a local array: a dynamically indexed
+    // array would give the kernel a stack frame)
+    auto hb_full = [&](int eb) { return eb ? c_full : e_full; };
+    auto hb_empty = [&](int eb) { return eb ? c_empty : e_empty; };
     if (warp == 0) {
       if (elect_one()) {
         int stage = 0, phase = 0;
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int i = 0; i < n_seg; ++i) {
           const int eb = i & 1;
           if (i >= 2) {
-            FF_TIMED(w_buf, mbar_wait_cluster(hb_empty[eb], ((i >> 1) - 1) & 1));
+            FF_TIMED(w_buf, mbar_wait_cluster(hb_empty(eb), ((i >> 1) - 1) & 1));
             tc_fence_after();
           }
           bool started = false;
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
           }
-          umma_commit_pair(hb_full[eb], kPairMask);
+          umma_commit_pair(hb_full(eb), kPairMask);
         }
         if (args.prof) {
           unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
       for (int i = 0; i < n_seg; ++i) {
         const int eb = i & 1;
-        mbar_wait_cluster(hb_full[eb], (i >> 1) & 1);
+        mbar_wait_cluster(hb_full(eb), (i >> 1) & 1);
         tc_fence_after();
         if (warp == 4 && lane_id() == 0 && i < 6) FF_STAMP(18 + i);  // diagnostics: segment i's MMAs done
         const Seg g = seg_of(i);
@@ -377,7 +384,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         // TMEM buffer free: tcgen05 loads waited + fenced; the arrive publishes no data
         tc_fence_before();
-        mbar_arrive_remote_relaxed(mapa(hb_empty[eb], lrank));
+        mbar_arrive_remote_relaxed(mapa(hb_empty(eb), lrank));
         // region complete: the barrier orders the 128 threads' stores before the
         // issuer's gpu-scope release (cumulative), no per-thread fence
         named_bar_sync(1, 128);

@@ -17,7 +17,7 @@ NFLUSH = 4 if 'deep' in ARGV else (0 if 'warm' in ARGV else 1)
 SHAPES = {"llama": (512,8192,2048,2048,2,True), "gpt67b": (512,16384,4096,4096,1,False),
           "gpt2s": (512,3072,768,768,3,False), "opt": (4096,8192,2048,2048,1,False)}
 for name, shape in ([] if 'probe' in ARGV else SHAPES.items() if 'opt' in ARGV else list(SHAPES.items())[:3]):
-    for mode, label in ((0, "coop"), (4, "no-coop")):
+    for mode, label in (((1 << 28), "empty"), ((1 << 28) | 4, "empty-nocoop")) if 'empty' in ARGV else ((0, "coop"), (4, "no-coop")):
         lib.ff_set_debug_mode(mode)
         A,B,B1,D,E,ch,kc,ws,t = setup(*shape,None,2)
         f=lambda: nat.check(lib.ff_chain_launch(ctypes.byref(ch),ctypes.byref(kc),ctypes.byref(t),ws.data_ptr(),ws.numel(),None))
@@ -28,6 +28,7 @@ for name, shape in ([] if 'probe' in ARGV else SHAPES.items() if 'opt' in ARGV e
         for it in range(8):
             ea = torch.cuda.Event(enable_timing=True); eb = torch.cuda.Event(enable_timing=True)
             for _ in range(NFLUSH): flush_buf.add_(1.0)
+            if 'spin' in ARGV: lib.ff_spin(ctypes.c_longlong(200000), 148, ctypes.c_void_p(stream))
             stamp(0); ea.record()
             lib.ff_set_profile_buffer(ctypes.c_void_p(buf.data_ptr())); f(); lib.ff_set_profile_buffer(None)
             eb.record(); stamp(1)
