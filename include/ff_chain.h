@@ -53,12 +53,17 @@ extern "C" {
 #define FF_LOWERING_SPATIAL_SPLIT 1
 #define FF_LOWERING_DOUBLED_K 2
 
+/* storage / MMA input type of a 2-byte chain (fp32 accumulation either way) */
+#define FF_DTYPE_BF16 0
+#define FF_DTYPE_F16 1
+
 /* ChainGraph (workload.py:75-110): kind, dims (m,n,k,l), activation. */
 typedef struct ffChainDesc {
   int32_t kind;
   int32_t activation;
   int64_t m, n, k, l;
-  int32_t element_size; /* bytes per stored scalar; only 2 (bf16) executes on the GPU */
+  int32_t element_size; /* bytes per stored scalar; only 2 (bf16 / fp16) executes on the GPU */
+  int32_t dtype;        /* FF_DTYPE_BF16 (default, 0) or FF_DTYPE_F16: A, B, D, E and the intermediate C */
 } ffChainDesc;
 
 /* FusionPlan (plan.py:121-165).  Dimension index order is (m, n, k, l) = DIMS. */
@@ -94,7 +99,7 @@ typedef struct ffKernelConfig {
 } ffKernelConfig;
 
 /* Tensors: row-major, the reference layouts (simulator.py:112-123):
- * A[m,k], B[k,n] (standard) or B0[k,n], B1[k,n] (gated), D[n,l], E[m,l]. bf16. */
+ * A[m,k], B[k,n] (standard) or B0[k,n], B1[k,n] (gated), D[n,l], E[m,l]; bf16 or fp16 (ffChainDesc.dtype). */
 typedef struct ffTensors {
   const void* a;
   const void* b;  /* B (standard) or B0 (gated) */
@@ -117,6 +122,7 @@ typedef struct ffTensors {
 typedef struct ffConvDesc {
   int32_t batch, h, w, ic, oc1, oc2, k1, k2;
   int32_t activation; /* FF_ACT_* applied between the convolutions (ReLU in the reference) */
+  int32_t dtype;      /* FF_DTYPE_BF16 or FF_DTYPE_F16 */
 } ffConvDesc;
 
 /* GEMM-chain view of a conv chain (m = batch*h*w unpadded). */

@@ -47,9 +47,16 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     return bits.astype(np.uint32).view(np.float32)
 
 
-def dense_chain(kind: str, activation: str, inputs: dict, bf16_intermediate: bool = False) -> np.ndarray:
+def round_f16(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even to IEEE half, returned as float32."""
+    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
+
+
+def dense_chain(kind: str, activation: str, inputs: dict, bf16_intermediate: bool = False,
+                f16_intermediate: bool = False) -> np.ndarray:
     """simulator.py:126-134: E = act(A@B)@D or (silu(A@B0) * (A@B1))@D, dense, no tiling.
-    ``bf16_intermediate`` rounds C to bf16 before the second GEMM (the GPU dataflow)."""
+    ``bf16_intermediate`` / ``f16_intermediate`` round C to the GPU's 2-byte storage type
+    before the second GEMM (the GPU dataflow)."""
     a = inputs["A"]
     if kind == "gated_ffn":
         c = silu(a @ inputs["B0"]) * (a @ inputs["B1"])
@@ -57,6 +64,8 @@ def dense_chain(kind: str, activation: str, inputs: dict, bf16_intermediate: boo
         c = _ACT[activation](a @ inputs["B"])
     if bf16_intermediate:
         c = round_bf16(c)
+    if f16_intermediate:
+        c = round_f16(c)
     return c @ inputs["D"]
 
 

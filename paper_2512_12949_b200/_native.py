@@ -27,6 +27,7 @@ KIND = {"standard_ffn": 0, "gated_ffn": 1}
 ACT = {"identity": 0, "relu": 1, "silu": 2, "gelu": 3}
 LOWERING = {"n/a": 0, "spatial_split": 1, "doubled_k": 2}
 XCHG_DSM, XCHG_L2, XCHG_L2_PAIR = 0, 1, 2
+DTYPE = {"bf16": 0, "f16": 1}
 
 # Exported symbols (must match include/ff_chain.h).
 EXPORTS = (
@@ -70,6 +71,7 @@ class ChainDesc(ctypes.Structure):
         ("k", ctypes.c_int64),
         ("l", ctypes.c_int64),
         ("element_size", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
     ]
 
 
@@ -108,7 +110,8 @@ class KernelConfig(ctypes.Structure):
 class ConvDesc(ctypes.Structure):
     """ffConvDesc: ConvChainConfig (workload.py:168-184) + batch and activation."""
 
-    _fields_ = [(name, ctypes.c_int32) for name in ("batch", "h", "w", "ic", "oc1", "oc2", "k1", "k2", "activation")]
+    _fields_ = [(name, ctypes.c_int32)
+                for name in ("batch", "h", "w", "ic", "oc1", "oc2", "k1", "k2", "activation", "dtype")]
 
 
 class Tensors(ctypes.Structure):

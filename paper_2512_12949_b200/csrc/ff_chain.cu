@@ -24,6 +24,10 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+CUtensorMapDataType elem_type(const ffChainDesc* ch) {
+  return ch->dtype == FF_DTYPE_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+}
+
 // ---------------------------------------------------------------------------
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 // ---------------------------------------------------------------------------
@@ -68,7 +72,8 @@ EncodeIm2colFn encode_im2col_fn() {
 // corners -pad / pad-(k1-1) make the traversal enumerate exactly the h x w
 // output positions; the tap offsets (s, r) then address the input pixel and
 // out-of-image taps read zeros.
-bool make_map_im2col(CUtensorMap* map, const void* ptr, int channels, int w, int h, int batch, int k) {
+bool make_map_im2col(CUtensorMap* map, const void* ptr, int channels, int w, int h, int batch, int k,
+                     CUtensorMapDataType dt) {
   EncodeIm2colFn fn = encode_im2col_fn();
   if (!fn) return false;
   const int pad = k / 2;
@@ -78,7 +83,7 @@ bool make_map_im2col(CUtensorMap* map, const void* ptr, int channels, int w, int
   int lower[2] = {-pad, -pad};
   int upper[2] = {pad - (k - 1), pad - (k - 1)};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, lower, upper, 64,
+  CUresult r = fn(map, dt, 4, const_cast<void*>(ptr), dims, strides, lower, upper, 64,
                   128, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
@@ -93,14 +98,14 @@ bool make_map_im2col(CUtensorMap* map, const void* ptr, int channels, int w, int
 
 // Row-major bf16 matrix [rows][cols] -> 2-D map with a (box_cols x box_rows) box, 128B swizzle.
 bool make_map(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
-              uint32_t box_rows) {
+              uint32_t box_rows, CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+  CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -274,24 +279,25 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   const WsLayout wl = ws_layout(ch, cfg, conv2);
   uint8_t* wsb = reinterpret_cast<uint8_t*>(ws);
   CUtensorMap mA, mB0, mB1, mD, mC, mCs;
-  bool ok = implicit ? make_map_im2col(&mA, t->a, conv->ic, conv->w, conv->h, conv->batch, conv->k1)
-                     : make_map(&mA, t->a, M, K, 64, 128);
-  ok = ok && make_map(&mB0, t->b, K, N, 64, 64);
-  ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64);
-  ok = ok && make_map(&mD, t->d, conv2 ? (uint64_t)conv->k2 * conv->k2 * N : N, L, 64, 64);
+  const CUtensorMapDataType dt = elem_type(ch);
+  bool ok = implicit ? make_map_im2col(&mA, t->a, conv->ic, conv->w, conv->h, conv->batch, conv->k1, dt)
+                     : make_map(&mA, t->a, M, K, 64, 128, dt);
+  ok = ok && make_map(&mB0, t->b, K, N, 64, 64, dt);
+  ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64, dt);
+  ok = ok && make_map(&mD, t->d, conv2 ? (uint64_t)conv->k2 * conv->k2 * N : N, L, 64, 64, dt);
   const bool l2x = (kMode == ff::XCHG_L2 && cfg->ring > 1);
   const bool cs = l2x || conv2;  // C scratch in use: [m_tiles*128][N] 2D view (publish stores, ring hops)
   ok = ok && make_map(&mCs, cs ? (const void*)(wsb + wl.c_off) : t->a, cs ? (uint64_t)cfg->m_tiles * 128 : M,
-                      cs ? N : K, 64, 128);
+                      cs ? N : K, 64, 128, dt);
   if (conv2)  // GEMM1 operand: the scratch as an NHWC map [batch][h][w][oc1], im2col boxes of the k2 x k2 window
-    ok = ok && make_map_im2col(&mC, wsb + wl.c_off, (int)N, conv->w, conv->h, conv->batch, conv->k2);
+    ok = ok && make_map_im2col(&mC, wsb + wl.c_off, (int)N, conv->w, conv->h, conv->batch, conv->k2, dt);
   else
     mC = mCs;
   CUtensorMap mE, mW;  // E tile outputs: bf16 E [M][L] box {64, 128}; fp32 split-N workspace [M][L] box {32, 128}
   {
     const uint64_t de[2] = {L, M}, se[1] = {L * 2};
     const uint32_t be[2] = {64, 128};
-    ok = ok && make_map_nd(&mE, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, t->e, de, se, be);
+    ok = ok && make_map_nd(&mE, dt, 2, t->e, de, se, be);
     const uint64_t sw[1] = {L * 4};
     const uint32_t bw[2] = {32, 128};
     ok = ok && make_map_nd(&mW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, wsb + wl.e_off, de, sw, bw);
@@ -347,6 +353,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
+  a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
   if (implicit || conv2) {
     a.conv_k1 = implicit ? conv->k1 : 0;
@@ -431,7 +438,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
       hit = true;
       break;
     }
-  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const auto BF = elem_type(ch);  // bf16 or fp16 storage
   bool ok = true;
   if (!hit) {
   {  // A [M][K] as {64, M, K/64}
@@ -530,6 +537,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
   a.dbg = g_dbg;
+  a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   // hops deferred past GEMM0(T+1): about one C drain (+ its store for the
   // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
   a.defer = cfg->ring - 1 - cfg->ring / 4;  // measured: 3/4 of the hops (profiles/r01/cfgs_defer.log)
@@ -638,7 +646,9 @@ int validate_chain(const ffChainDesc* ch) {
   if (!ch) return fail(FF_ERR_ARG, "null chain descriptor");
   if (ch->kind != FF_KIND_STANDARD && ch->kind != FF_KIND_GATED) return fail(FF_ERR_ARG, "unknown chain kind");
   if (ch->activation < 0 || ch->activation > FF_ACT_GELU_TANH) return fail(FF_ERR_ARG, "unknown activation");
-  if (ch->element_size != 2) return fail(FF_ERR_UNSUPPORTED, "GPU path executes bf16 storage (element_size 2) only");
+  if (ch->element_size != 2)
+    return fail(FF_ERR_UNSUPPORTED, "GPU path executes 2-byte storage (bf16 / fp16, element_size 2) only");
+  if (ch->dtype != FF_DTYPE_BF16 && ch->dtype != FF_DTYPE_F16) return fail(FF_ERR_ARG, "unknown dtype");
   if (ch->m < 1 || ch->n < 64 || ch->k < 64 || ch->l < 64)
     return fail(FF_ERR_UNSUPPORTED, "extents below one 64-wide tile");
   if (ch->k % 64 || ch->n % 64 || ch->l % 64)
@@ -894,6 +904,7 @@ int ff_conv_chain_desc(const ffConvDesc* cv, ffChainDesc* out) {
   ch.k = (int64_t)cv->k1 * cv->k1 * cv->ic;
   ch.l = cv->oc2;
   ch.element_size = 2;
+  ch.dtype = cv->dtype;
   *out = ch;
   return validate_chain(&ch);
 }

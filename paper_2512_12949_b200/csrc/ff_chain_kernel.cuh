@@ -82,6 +82,7 @@ struct ChainArgs {
   // block of C) reads an im2col box of it once the halo tiles are published
   int conv2_k;
   int conv2_cblk;      // oc1 / 64
+  int f16;             // 2-byte storage is fp16 (else bf16): MMA input format, C / E packing
   uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits
   unsigned long long* prof;  // optional diagnostics: per CTA [FF_PROF_STRIDE] = 16 wait-cycle counters + 16 globaltimer stamps
 };
@@ -201,7 +202,7 @@ __device__ __forceinline__ void split_finish(const ChainArgs& args, uint32_t* co
       const int r = row0 + r_lo + idx / kV;
       if (idx < n4 && r < args.M) {
         const size_t off = (size_t)r * args.L + col0 + 4 * (idx % kV);
-        *reinterpret_cast<uint2*>(args.E + off) = make_uint2(pack_bf16x2(f[j].x, f[j].y), pack_bf16x2(f[j].z, f[j].w));
+        *reinterpret_cast<uint2*>(args.E + off) = make_uint2(pack2(args.f16, f[j].x, f[j].y), pack2(args.f16, f[j].z, f[j].w));
         *reinterpret_cast<float4*>(args.ws + off) = z;
       }
     }
@@ -464,8 +465,8 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
-      constexpr uint32_t idesc0 = idesc_bf16(128, kNB, 0, 1);
-      constexpr uint32_t idesc1 = idesc_bf16(128, kLB, 0, 1);
+      const uint32_t idesc0 = idesc_as(idesc_bf16(128, kNB, 0, 1), args.f16);
+      const uint32_t idesc1 = idesc_as(idesc_bf16(128, kLB, 0, 1), args.f16);
       auto gemm0 = [&](int T, int kb0, int kb1) {
         const int cb = T & 1;
         if (kb0 == 0) {
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         uint32_t pk[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+        for (int i = 0; i < 8; ++i) pk[i] = pack2(args.f16, v[2 * i], v[2 * i + 1]);
         const int sub = c0 / 64;
         const int ch = (c0 % 64) / 8;  // 16-byte chunk inside the 128-byte row
         const uint32_t rowb = own_slot + sub * (C::BM * C::BK * 2) + row * 128;
@@ -702,7 +703,7 @@ __global__ void __launch_bounds__(256, 1)
             } else {
               uint32_t pk[8];
 #pragma unroll
-              for (int i = 0; i < 8; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              for (int i = 0; i < 8; ++i) pk[i] = pack2(args.f16, v[2 * i], v[2 * i + 1]);
               const int j0 = (c0 % 64) / 8;
               st_shared_v4(rowb + ((j0 ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
               st_shared_v4(rowb + (((j0 + 1) ^ (row & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);

@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     } else if (warp == 1) {
       if (leader && elect_one()) {
-        constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
+        const uint32_t idesc1 = idesc_as(idesc_bf16(256, kLB, 0, 1), args.f16);
         int stage = 0, phase = 0;
         unsigned long long w_full = 0, w_buf = 0;
         const unsigned long long t_start = clock64();
@@ -531,8 +531,8 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       };
-      constexpr uint32_t idesc0 = idesc_bf16(256, C::kN0, 0, 1);
-      constexpr uint32_t idesc1 = idesc_bf16(256, kLB, 0, 1);
+      const uint32_t idesc0 = idesc_as(idesc_bf16(256, C::kN0, 0, 1), args.f16);
+      const uint32_t idesc1 = idesc_as(idesc_bf16(256, kLB, 0, 1), args.f16);
       auto gemm0 = [&](int T, int kb0, int kb1) {
         if (kb0 >= kb1) return;
         if (kb0 == 0) {
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           uint32_t pk[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+          for (int i = 0; i < 16; ++i) pk[i] = pack2(args.f16, v[2 * i], v[2 * i + 1]);
           const uint32_t tile = own_slot + ((c0 - r0) / 64) * 16384;
           const int ch = (c0 % 64) / 8;
 #pragma unroll
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(256, 1)
             if (bf16_out) {
               uint32_t pk[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              for (int i = 0; i < 16; ++i) pk[i] = pack2(args.f16, v[2 * i], v[2 * i + 1]);
               const int ch = (c0 % 64) / 8;
 #pragma unroll
               for (int j = 0; j < 4; ++j)
@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(256, 1)
             if (bf16_out) {
               uint32_t pk[16];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+              for (int i = 0; i < 16; ++i) pk[i] = pack2(args.f16, v[2 * i], v[2 * i + 1]);
               const int ch = (c0 % 64) / 8;
 #pragma unroll
               for (int j = 0; j < 4; ++j)
@@ -955,7 +955,7 @@ __global__ void __launch_bounds__(256, 1)
         const int ch = (c % 16) / 2;
         *reinterpret_cast<uint2*>(smem_gen + (ebuf - base) + (c / 16) * (R * 128) + rr * 128 + ((ch ^ (rr & 7)) << 4) +
                                   (c & 1) * 8) =
-            make_uint2(pack_bf16x2(acc[q4].x, acc[q4].y), pack_bf16x2(acc[q4].z, acc[q4].w));
+            make_uint2(pack2(args.f16, acc[q4].x, acc[q4].y), pack2(args.f16, acc[q4].z, acc[q4].w));
       }
     }
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 22] = globaltimer_ns();

@@ -537,6 +537,19 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// two fp32 -> one packed pair of the chain's 2-byte storage type
+__device__ __forceinline__ uint32_t pack2(bool f16, float lo, float hi) {
+  return f16 ? pack_f16x2(lo, hi) : pack_bf16x2(lo, hi);
+}
+// instruction descriptor of a bf16 MMA switched to fp16 A/B (kind::f16: format 0 = f16, 1 = bf16)
+__host__ __device__ constexpr uint32_t idesc_as(uint32_t idesc, bool f16) {
+  return f16 ? (idesc & ~((1u << 7) | (1u << 10))) : idesc;
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");

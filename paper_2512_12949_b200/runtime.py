@@ -19,9 +19,22 @@ from .workload import DIMS, GATED_FFN, ChainGraph, ConvBlockConfig, ConvChainCon
 _workspaces: dict = {}
 
 
-def chain_desc(graph: ChainGraph) -> nat.ChainDesc:
+def chain_desc(graph: ChainGraph, dtype: str = "bf16") -> nat.ChainDesc:
     d = graph.dims
-    return nat.ChainDesc(nat.KIND[graph.kind], nat.ACT[graph.activation], d.m, d.n, d.k, d.l, d.element_size)
+    return nat.ChainDesc(nat.KIND[graph.kind], nat.ACT[graph.activation], d.m, d.n, d.k, d.l, d.element_size,
+                         nat.DTYPE[dtype])
+
+
+def _storage(tensors) -> str:
+    """'bf16' or 'f16': every chain tensor must share one 2-byte storage type."""
+    import torch
+
+    kinds = {t.dtype for t in tensors}
+    if kinds == {torch.bfloat16}:
+        return "bf16"
+    if kinds == {torch.float16}:
+        return "f16"
+    raise ValueError(f"chain tensors must all be bfloat16 or all float16, got {sorted(map(str, kinds))}")
 
 
 def plan_desc(plan: FusionPlan) -> nat.PlanDesc:
@@ -109,16 +122,19 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
     names = ("A", "B0", "B1", "D") if gated else ("A", "B", "D")
     d = graph.dims
     shapes = {"A": (d.m, d.k), "B": (d.k, d.n), "B0": (d.k, d.n), "B1": (d.k, d.n), "D": (d.n, d.l)}
+    storage = _storage([tensors[n] for n in names])
     for name in names:
         t = tensors[name]
-        if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
+        if not t.is_cuda or tuple(t.shape) != shapes[name] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]}")
         if t.data_ptr() % 16:
             raise ValueError(f"{name} must be 16-byte aligned")
     a = tensors["A"]
     if out is None:
-        out = torch.empty((d.m, d.l), dtype=torch.bfloat16, device=a.device)
-    ch = chain_desc(graph)
+        out = torch.empty((d.m, d.l), dtype=a.dtype, device=a.device)
+    elif out.dtype != a.dtype:
+        raise ValueError("out must have the inputs' dtype")
+    ch = chain_desc(graph, storage)
     ws_bytes = lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(cfg))
     s = stream if stream is not None else torch.cuda.current_stream(a.device)
     if not hasattr(s, "cuda_stream"):
@@ -204,9 +220,10 @@ def profile_configs(graph: ChainGraph, cfgs, tensors: dict, iters: int = 10, war
 # ----------------------------------------------------------------------------- conv chains
 
 
-def conv_desc(cfg, batch: int = 1, activation: str = "relu") -> nat.ConvDesc:
+def conv_desc(cfg, batch: int = 1, activation: str = "relu", dtype: str = "bf16") -> nat.ConvDesc:
     """ffConvDesc of a ConvChainConfig (reference) or ConvBlockConfig (k2 > 1 extension)."""
-    return nat.ConvDesc(batch, cfg.h, cfg.w, cfg.ic, cfg.oc1, cfg.oc2, cfg.k1, cfg.k2, nat.ACT[activation])
+    return nat.ConvDesc(batch, cfg.h, cfg.w, cfg.ic, cfg.oc1, cfg.oc2, cfg.k1, cfg.k2, nat.ACT[activation],
+                        nat.DTYPE[dtype])
 
 
 def lower_conv(cfg, batch: int = 1, exchange: str = "auto", activation: str = "relu",
@@ -241,12 +258,13 @@ def launch_conv(cfg, kcfg: nat.KernelConfig, x, w1, w2, out=None, stream=None, a
     batch = x.shape[0]
     w2_shape = (cfg.oc1, cfg.oc2) if cfg.k2 == 1 else (cfg.k2, cfg.k2, cfg.oc1, cfg.oc2)
     shapes = {"x": (batch, cfg.h, cfg.w, cfg.ic), "w1": (cfg.k1, cfg.k1, cfg.ic, cfg.oc1), "w2": w2_shape}
+    storage = _storage([x, w1, w2])
     for name, t in (("x", x), ("w1", w1), ("w2", w2)):
-        if not t.is_cuda or t.dtype != torch.bfloat16 or tuple(t.shape) != shapes[name] or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous bf16 CUDA tensor of shape {shapes[name]}")
+        if not t.is_cuda or tuple(t.shape) != shapes[name] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]}")
     if out is None:
-        out = torch.empty((batch, cfg.h, cfg.w, cfg.oc2), dtype=torch.bfloat16, device=x.device)
-    cd = conv_desc(cfg, batch, activation)
+        out = torch.empty((batch, cfg.h, cfg.w, cfg.oc2), dtype=x.dtype, device=x.device)
+    cd = conv_desc(cfg, batch, activation, storage)
     ws_bytes = lib.ff_conv_chain_workspace_bytes(ctypes.byref(cd), ctypes.byref(kcfg))
     s = stream if stream is not None else torch.cuda.current_stream(x.device)
     ws = _workspace(ws_bytes, x.device, s)

@@ -314,3 +314,39 @@ def test_workspace_zero_invariant_across_configs():
                 cnt = ws[(1 << 20):(1 << 20) + (256 << 10)]
                 zone = ws[(1 << 20) + (256 << 10):(1 << 20) + (256 << 10) + (32 << 20)]
                 assert int((cnt != 0).sum()) == 0 and int((zone != 0).sum()) == 0, (case, exchange, cfg.as_dict())
+
+
+F16_CASES = [
+    ("gated_ffn", "silu", 512, 8192, 2048, 2048),      # LLaMA-1B shape
+    ("standard_ffn", "relu", 512, 16384, 4096, 4096),  # GPT-6.7B shape
+    ("standard_ffn", "gelu", 200, 768, 256, 768),
+]
+
+
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("case", F16_CASES, ids=lambda c: f"{c[0][:3]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
+def test_fp16_chain_matches_oracle(case, exchange):
+    """fp16 storage (north star: bf16/fp16 with fp32 accumulation).  Weights are
+    scaled by 1/sqrt(fan-in) so C and E stay inside the fp16 range."""
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    try:
+        cfg = runtime.lower(graph, None, 148, exchange)
+    except nat.UnsupportedPlan:
+        pytest.skip(f"{exchange} has no lowering for {case}")
+    raw = oracle.make_inputs(kind, m, n, k, l, seed=4)
+    scale = {"A": 1.0, "B": k ** -0.5, "B0": k ** -0.5, "B1": k ** -0.5, "D": n ** -0.5}
+    host = {name: oracle.round_f16(v * scale[name]) for name, v in raw.items()}
+    dev = {name: torch.from_numpy(v).cuda().to(torch.float16) for name, v in host.items()}
+    out = runtime.launch(graph, cfg, dev)
+    torch.cuda.synchronize()
+    assert out.dtype == torch.float16
+    got = out.float().cpu().numpy()
+    ref_h = oracle.dense_chain(kind, act, host, f16_intermediate=True)
+    ref = oracle.dense_chain(kind, act, host)
+    assert np.isfinite(got).all()
+    assert oracle.max_relative_error(got, ref_h) <= TOL and oracle.max_relative_error(got, ref) <= TOL
