@@ -41,7 +41,24 @@ WORKLOADS = {
     "gpt67b": ("standard_ffn", "relu", 512, 16384, 4096, 4096, "GPT-6.7B FFN M=512, 4096->16384->4096"),
     "gpt2s": ("standard_ffn", "gelu", 512, 3072, 768, 768, "GPT-2 small FFN M=512, 768->3072->768, GELU"),
     "opt13b_m4096": ("standard_ffn", "relu", 4096, 8192, 2048, 2048, "OPT-1.3B FFN M=4096 (per-GPU shard of 32768/8)"),
+    # BASELINE.json configs[4] as a strong-scaling sweep: M=32768 tokens in total, rank r of N
+    # runs the r-th contiguous shard of 32768/N rows (bench.py --workload opt13b_m32768 --gpus N)
+    "opt13b_m32768": ("standard_ffn", "relu", 32768, 8192, 2048, 2048,
+                      "OPT-1.3B FFN M=32768 tokens in total, token-sharded across the GPUs (strong scaling)"),
 }
+STRONG = {"opt13b_m32768"}  # workloads whose M is the job total, split across ranks
+
+
+def rank_rows(name, world, rank=0):
+    """Token rows this rank processes: the whole M (weak scaling: every rank its own
+    batch) or its contiguous shard of the total (strong scaling, sharding.shard_bounds)."""
+    m = WORKLOADS[name][2]
+    if name not in STRONG or world == 1:
+        return m
+    from paper_2512_12949_b200 import sharding
+
+    lo, hi = sharding.shard_bounds(m, world, rank)
+    return hi - lo
 DEFAULT_WORKLOAD = "llama1b"
 
 
@@ -266,30 +283,36 @@ def make_device_inputs(kind, m, n, k, l, seed, device):
     return t
 
 
-def graph_of(name):
+def graph_of(name, m=None):
     from paper_2512_12949_b200 import workload as W
 
-    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    kind, act, m0, n, k, l, _ = WORKLOADS[name]
+    m = m0 if m is None else m
     dims = W.DimensionSpec(m, n, k, l, 2)
     return W.build_gated_ffn(dims) if kind == "gated_ffn" else W.build_standard_ffn(dims, act)
 
 
-def choose_config(name, tensors, profile=True):
+def choose_config(name, tensors, profile=True, m=None):
     """Plan -> physical launch: top-K reference plans (plan cache) lowered and timed
     on the device (ProfileBestFromList), plus the runtime's hardware-shaped config.
     profile=False (ncu launch lists): the shipped M-bin dispatch table's entry."""
+    m = WORKLOADS[name][2] if m is None else m
     if not profile:
         from paper_2512_12949_b200 import dispatch
 
-        fam = {"llama1b": "llama1b", "gpt67b": "gpt67b", "gpt2s": "gpt2s", "opt13b_m4096": "opt13b"}[name]
-        m = WORKLOADS[name][2]
-        cfg = dispatch.shipped(fam).config_for(m)
-        return cfg, f"dispatch table [{fam}, M bin of {m}]", []
+        fam = {"llama1b": "llama1b", "gpt67b": "gpt67b", "gpt2s": "gpt2s", "opt13b_m4096": "opt13b",
+               "opt13b_m32768": "opt13b"}[name]
+        table = dispatch.shipped(fam)
+        if m <= table.bins[-1]:
+            return table.config_for(m), f"dispatch table [{fam}, M bin of {m}]", []
+        from paper_2512_12949_b200 import runtime
+
+        return runtime.lower(graph_of(name, m), None), "runtime-auto (beyond the dispatch table)", []
     from paper_2512_12949_b200 import plan_cache, runtime
     from paper_2512_12949_b200.plan import plan_from_dict
 
-    graph = graph_of(name)
-    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    graph = graph_of(name, m)
+    kind, act, _, n, k, l, _ = WORKLOADS[name]
     cands = []
     entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
     plans = [plan_from_dict(p) for p in entry["top"]] if entry else []
@@ -339,8 +362,10 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     name = args.workload
-    kind, act, m, n, k, l, desc = WORKLOADS[name]
-    graph = graph_of(name)
+    kind, act, m_total, n, k, l, desc = WORKLOADS[name]
+    strong = name in STRONG
+    m = rank_rows(name, world, rank)
+    graph = graph_of(name, m)
     tensors = make_device_inputs(kind, m, n, k, l, seed=1234 + rank, device=dev)
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -348,7 +373,7 @@ def run_ours(args, rank, world, local_rank):
         flush_buf.add_(1.0)
 
     stream = torch.cuda.current_stream(dev)
-    cfg, cfg_name, candidates = choose_config(name, tensors, profile=not args.no_profile_plans)
+    cfg, cfg_name, candidates = choose_config(name, tensors, profile=not args.no_profile_plans, m=m)
     out = torch.empty((m, l), dtype=torch.bfloat16, device=dev)
 
     def step():
@@ -376,7 +401,8 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         total_ms = _max_over_ranks(total_ms, dev)
     fl = flops_of(kind, m, n, k, l)
-    value = fl * args.steps * world / (total_ms * 1e-3) / 1e12
+    job_fl = flops_of(kind, m_total, n, k, l) if strong else fl * world  # whole-job work per step
+    value = job_fl * args.steps / (total_ms * 1e-3) / 1e12
     ms_step = total_ms / args.steps
 
     # e2e through the public API: pinned host A -> device, chain, E -> pinned host
@@ -398,7 +424,7 @@ def run_ours(args, rank, world, local_rank):
     e2e_ms = float(sum(e2e_times))
     if world > 1:
         e2e_ms = _max_over_ranks(e2e_ms, dev)
-    e2e_value = fl * args.steps * world / (e2e_ms * 1e-3) / 1e12
+    e2e_value = job_fl * args.steps / (e2e_ms * 1e-3) / 1e12
 
     # unfused cuBLAS on the same config
     cub = cublas_unfused(kind, act, tensors, flush, stream, max(args.steps, 5))
@@ -420,12 +446,13 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic U[-1,1] bf16 inputs and weights (seeded)",
         "config": {"workload": desc, "m_per_gpu": m, "n": n, "k": k, "l": l, "kind": kind, "activation": act,
-                   "global_batch_tokens": m * world, "parallelism": f"token-sharded x{world} (independent per GPU)",
+                   "global_batch_tokens": m_total if strong else m * world,
+                   "parallelism": f"token-sharded x{world} (independent per GPU)",
                    "l2": "flushed between timed steps (256 MiB write)", "launch": cfg.as_dict(),
                    "plan": cfg_name, "candidates_ms": candidates},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
