@@ -14,7 +14,7 @@ import threading
 from .errors import CapacityExceeded, FusePlanError, PlanError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libff_chain.so")
+LIB_PATH = os.environ.get("FF_CHAIN_LIB") or os.path.join(_HERE, "libff_chain.so")  # FF_CHAIN_LIB: A/B builds
 
 FF_OK = 0
 FF_ERR_PLAN = 1

@@ -204,8 +204,8 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
   // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
   w.s_off = off;
-  if (pair && c->n_splits > 1)
-    off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * 256 * ch->l * sizeof(float));
+  if (c->n_splits > 1)  // split-N exchange regions (pair kernel, and the 1-CTA kernels' final units)
+    off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * (pair ? 256 : 128) * ch->l * sizeof(float));
   // helper pairs' E partials, one region per (E tile, n-step); plain stores, no zero invariant
   w.h_off = off;
   if (pair && c->helpers > 0) off = align256(off + (size_t)c->steps * c->m_tiles * 256 * ch->l * sizeof(float));
@@ -294,6 +294,8 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   else
     mC = mCs;
   CUtensorMap mE, mW;  // E tile outputs: bf16 E [M][L] box {64, 128}; fp32 split-N workspace [M][L] box {32, 128}
+  CUtensorMap mSlab, mEr;  // split-N exchange regions / E row slices (final-unit reduce-scatter)
+  const int S = std::max(1, cfg->n_splits), R = 128 / S;
   {
     const uint64_t de[2] = {L, M}, se[1] = {L * 2};
     const uint32_t be[2] = {64, 128};
@@ -301,6 +303,15 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     const uint64_t sw[1] = {L * 4};
     const uint32_t bw[2] = {32, 128};
     ok = ok && make_map_nd(&mW, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, wsb + wl.e_off, de, sw, bw);
+    const uint64_t tiles = (uint64_t)cfg->m_tiles * (L / kLB);
+    const uint64_t ds[3] = {32, 16, tiles * S * (kLB / 4)}, ss[2] = {128, 2048};
+    const uint32_t bs[3] = {32, (uint32_t)std::max(1, R / 8), kLB / 4};
+    ok = ok && make_map_nd(&mSlab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, cfg->n_splits > 1 ? (const void*)(wsb + wl.s_off)
+                                                                                        : t->e,
+                           ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const uint64_t dr[3] = {64, M, L / 64}, sr[2] = {L * 2, 128};
+    const uint32_t br[3] = {64, (uint32_t)std::min(128, R), kLB / 64};
+    ok = ok && make_map_nd(&mEr, dt, 3, t->e, dr, sr, br);
   }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
@@ -355,6 +366,16 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.dbg = g_dbg;
   a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
+  a.slab = reinterpret_cast<float*>(wsb + wl.s_off);
+  // final-unit split-N reduce-scatter through exchange regions (debug bit 29, opt-in): one
+  // unit per ring, 8-row slices, the S slots (the whole fp32 tile) in the drained stages
+  // and the bf16 row slice in the own slot.  Measured slower than the TMA reduce-add +
+  // last-arriver finish for GPT-2s (29.7 vs 26.6 us, profiles/r01/timeline_gpt2s_regions.log):
+  // with S = 8 both move ~11-13 MB of fp32 partials into a dirty L2 at once, and the
+  // region path adds the partner loads
+  a.finish_tma = S > 1 && S <= 8 && 128 % S == 0 && R % 8 == 0 && cfg->units <= rings && !conv2 &&
+                 (size_t)128 * kLB * 4 <= (size_t)C::kOFF_OWN && (size_t)R * kLB * 2 <= (size_t)C::kCHUNK_BYTES &&
+                 (size_t)cfg->m_tiles * (L / kLB) * 16 <= (1u << 17) && (g_dbg & (1u << 29));
   if (implicit || conv2) {
     a.conv_k1 = implicit ? conv->k1 : 0;
     a.conv_H = conv->h;
@@ -368,7 +389,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, mE, mW, a);
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, mE, mW, mSlab, mEr, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
   return FF_OK;

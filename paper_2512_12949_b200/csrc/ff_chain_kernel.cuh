@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(256, 1)
                     const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmD,
                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmCs,
                     const __grid_constant__ CUtensorMap tmE, const __grid_constant__ CUtensorMap tmW,
+                    const __grid_constant__ CUtensorMap tmSlab, const __grid_constant__ CUtensorMap tmEr,
                     const ChainArgs args) {
   using C = ChainCfg<kGated, kNB, kLB, kStages, kMode>;
   constexpr bool kDSM = (kMode == XCHG_DSM);
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
+  if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;
   const uint32_t p = kDSM ? cluster_rank() : (uint32_t)(blockIdx.x % G);  // ring position
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t own_full = bx + 32, own_free = bx + 40;
   const uint32_t recv_full[2] = {bx + 48, bx + 56};
   const uint32_t recv_used[2] = {bx + 64, bx + 72};
-  const uint32_t e_full = bx + 80, e_empty = bx + 88;
+  const uint32_t e_full = bx + 80, e_empty = bx + 88, e_load = bx + 96;
   auto counter = [&](int h) { return bx + 104 + 4u * h; };  // 16 u32 counters
   const uint32_t ack_count = counter(0);                    // DSM: landed-chunk acks
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
@@ -315,6 +317,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(own_free, (G == 1 && args.conv2_k <= 1) ? 1 : 2);
     mbar_init(e_full, 1);
     mbar_init(e_empty, 128);
+    mbar_init(e_load, 1);
     fence_mbar_init();
     if (kDSM)
       for (int b = 0; b < 2; ++b) mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+  if (threadIdx.x == 0) FF_STAMP(17);
 
   // slot h of global step T holds GEMM0 k-blocks [h*KB/G, (h+1)*KB/G) of step T+1
   auto slot_lo = [&](int h) { return h * kblocks / G; };
@@ -618,6 +622,7 @@ __global__ void __launch_bounds__(256, 1)
       const int t = T % steps;
       const int cb = T & 1;
       FF_TIMED(w_cfull, mbar_wait(c_full[cb], (T >> 1) & 1));
+      if (warp == 4 && lane_id() == 0 && T == 0) FF_STAMP(18);  // C chunk 0 accumulated
       tc_fence_after();
       FF_TIMED(w_ofree, mbar_wait(own_free, (T & 1) ^ 1));
       const uint32_t tacc = lane_base + cb * C::kAcc;
@@ -671,27 +676,140 @@ __global__ void __launch_bounds__(256, 1)
         // E tile of this unit: TMEM -> registers -> global
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait(e_full, (T / steps) & 1);
+        if (warp == 4 && lane_id() == 0) FF_STAMP(30);  // E accumulated (last hop)
         tc_fence_after();
         // E tile through the own slot (free once hop 0, the pushes / the C store are done)
         // in SW128 16 KB tiles, leaving by bulk tensor ops: bf16 TMA stores (S == 1) or
         // fp32 TMA reduce-adds into the split-N workspace (per-thread rows would be 32
         // scattered lines per warp access; measured ~16 GB/s per SM with red.global.add)
-        mbar_wait(own_free, T & 1);
         const bool f32 = args.S > 1;
         const int cpt = f32 ? 32 : 64;  // columns per 16 KB tile
         // the ring's final unit stages the whole tile at once in the drained pipeline
-        // stages (no load follows); earlier units use the own slot in rounds
+        // stages (no load follows); earlier units use the own slot in rounds, once it
+        // is free (hop 0 read it, pushes acked / C store done)
         const bool final_unit = (T / steps) == my_units - 1;
+        const bool issuer = (warp == 4 && lane_id() == 0);
+        if (final_unit && args.finish_tma) {
+          // Split-N reduce-scatter through exchange regions (as the pair kernel's tail):
+          // row slice j (R = 128/S rows) of the E tile belongs to split j; rows of other
+          // slices go from TMEM registers straight to this split's region as coalesced
+          // 512-byte warp stores ([16-byte chunk][128 rows]), own rows to shared memory;
+          // after the (tile, split) flags the partners' rows arrive by TMA (128-byte inner
+          // boxes), the S partials are summed in split order (deterministic) and one TMA
+          // store writes the rows.  No atomics: measured 12.6 MB of TMA reduce-adds for
+          // GPT-2s took ~4.5 us of L2 reduction throughput.
+          const int S = args.S, R = C::BM / S;
+          const int sp = u.id / (args.m_tiles * args.l_clusters);  // this unit's split
+          const int tile = (u.m0 / C::BM) * (args.L / kLB) + u.l0 / kLB;
+          constexpr int kChunks = kLB / 4;
+          const int slice = row / R;
+          float* const dst = args.slab + ((size_t)tile * S + sp) * (kChunks * 128 * 4) + row * 4;
+          const uint32_t own_row = base + sp * (R * kChunks * 16) + (row - sp * R) * 16;
+          auto put16 = [&](int c0, const float* v) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int ch = c0 / 4 + j;
+              if (slice != sp)
+                st_global_v4(dst + (size_t)ch * 512, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+              else
+                st_shared_v4(own_row + ch * (R * 16), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                             __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            }
+          };
+#pragma unroll 1
+          for (int c0 = 0; c0 < kLB;) {
+            if (kLB - c0 >= 64) {
+              float v[32], w[32];
+              tmem_ld32x2(lane_base + C::kTMEM_E + c0, lane_base + C::kTMEM_E + c0 + 32, v, w);
+              put16(c0, v);
+              put16(c0 + 16, v + 16);
+              put16(c0 + 32, w);
+              put16(c0 + 48, w + 16);
+              c0 += 64;
+            } else {
+              float v[16];
+              tmem_ld16(lane_base + C::kTMEM_E + c0, v);
+              put16(c0, v);
+              c0 += 16;
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(e_empty);
+          named_bar_sync(1, 128);  // all region stores issued before the issuer's release (cumulative)
+          if (issuer) FF_STAMP(24);
+          uint32_t* const flags = args.flags + (1u << 17) + tile * 16;
+          if (issuer) {
+            st_release_gpu_u32(flags + sp, args.epoch);
+            uint32_t polls = 0;
+            for (int j = 0; j < S; ++j) {
+              if (j == sp) continue;
+              while ((int)(ld_relaxed_gpu_u32(flags + j) - args.epoch) < 0)
+                if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+            }
+            fence_acq_rel_gpu();
+            fence_proxy_async_global();
+            if (args.prof) args.prof[blockIdx.x * FF_PROF_STRIDE + 25] = globaltimer_ns();
+            mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kChunks * 16));
+            for (int j = 0; j < S; ++j)
+              if (j != sp)
+                tma_load_3d(base + j * (R * kChunks * 16), &tmSlab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
+          }
+          mbar_wait(own_free, T & 1);  // the own slot stages the bf16 rows (DSM pushes read it until acked)
+          mbar_wait(e_load, 0);
+          // sum in split order, cast, stage [kLB/64][R][128 B] SW128 for one TMA store
+          const uint8_t* const src = smem_gen;
+          const uint32_t ebuf = own_slot;
+          const int n_items = R * kChunks;
+#pragma unroll 1
+          for (int it0 = row; it0 < n_items; it0 += 512) {
+            float4 acc[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+              acc[q4] = it0 + 128 * q4 < n_items ? *reinterpret_cast<const float4*>(src + (it0 + 128 * q4) * 16)
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int j = 1; j < S; ++j) {
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                if (it0 + 128 * q4 >= n_items) continue;
+                const float4 f = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + (it0 + 128 * q4) * 16);
+                acc[q4].x += f.x;
+                acc[q4].y += f.y;
+                acc[q4].z += f.z;
+                acc[q4].w += f.w;
+              }
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int it = it0 + 128 * q4;
+              if (it >= n_items) continue;
+              const int c = it / R, rr = it % R;
+              const int ch = (c % 16) / 2;
+              *reinterpret_cast<uint2*>(smem_gen + (ebuf - base) + (c / 16) * (R * 128) + rr * 128 +
+                                        ((ch ^ (rr & 7)) << 4) + (c & 1) * 8) =
+                  make_uint2(pack2(args.f16, acc[q4].x, acc[q4].y), pack2(args.f16, acc[q4].z, acc[q4].w));
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (issuer) {
+            tma_store_3d(&tmEr, ebuf, 0, u.m0 + sp * R, u.l0 / 64);
+            bulk_commit();
+            FF_STAMP(26);
+          }
+          if (args.prof) t_e += clock64() - t_e0;
+          continue;
+        }
+        if (!final_unit) mbar_wait(own_free, T & 1);
         const uint32_t stg = final_unit ? base : own_slot;
         const int tpr = final_unit ? (C::kOFF_OWN / 16384) : (C::kCHUNK_BYTES / 16384);  // tiles per round
-        const bool issuer = (warp == 4 && lane_id() == 0);
 #pragma unroll 1
         for (int g0 = 0; g0 < kLB; g0 += cpt * tpr) {
           const int g1 = min(kLB, g0 + cpt * tpr);
 #pragma unroll 1
-          for (int c0 = g0; c0 < g1; c0 += 16) {
-            float v[16];
-            tmem_ld16(lane_base + C::kTMEM_E + c0, v);
+          // 16 columns of this thread's row into the SW128 staging tile
+          auto stage16 = [&](int c0, const float* v) {
             const uint32_t rowb = stg + ((c0 - g0) / cpt) * 16384 + row * 128;
             if (f32) {
               const int j0 = (c0 % 32) / 4;
@@ -708,6 +826,12 @@ __global__ void __launch_bounds__(256, 1)
               st_shared_v4(rowb + ((j0 ^ (row & 7)) << 4), pk[0], pk[1], pk[2], pk[3]);
               st_shared_v4(rowb + (((j0 + 1) ^ (row & 7)) << 4), pk[4], pk[5], pk[6], pk[7]);
             }
+          };
+#pragma unroll 1
+          for (int c0 = g0; c0 < g1; c0 += 16) {
+            float v[16];
+            tmem_ld16(lane_base + C::kTMEM_E + c0, v);
+            stage16(c0, v);
           }
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
@@ -726,9 +850,11 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
         mbar_arrive(e_empty);
+        if (warp == 4 && lane_id() == 0) FF_STAMP(24);  // E staged and its bulk ops issued
         if (args.S > 1)
           split_finish<kLB>(args, args.tile_cnt + (u.m0 / C::BM) * (args.L / kLB) + u.l0 / kLB, tmem_slot + 8,
                             issuer, true, u.m0, row, u.l0, 1, args.n_units <= args.n_rings);
+        if (warp == 4 && lane_id() == 0) FF_STAMP(26);  // split-N finish done
         if (args.prof) t_e += clock64() - t_e0;
       }
     }
@@ -744,6 +870,7 @@ __global__ void __launch_bounds__(256, 1)
 
   __syncthreads();
   if (kDSM) cluster_sync();  // no CTA leaves while a peer may still push or credit
+  if (threadIdx.x == 0) FF_STAMP(31);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::kTMEM_COLS>(tmem_base);

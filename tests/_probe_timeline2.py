@@ -15,7 +15,8 @@ mode = int(ARGV[1]) if len(ARGV) > 1 and ARGV[1].isdigit() else 0
 sel = [a for a in ARGV[1:] if a in SHAPES] or ["gpt67b", "llama"]
 for name in sel:
     lib.ff_set_debug_mode(mode)
-    A,B,B1,D,E,ch,kc,ws,t = setup(*SHAPES[name],None,2)
+    XCHG = 0 if 'x0' in ARGV else (1 if 'x1' in ARGV else 2)
+    A,B,B1,D,E,ch,kc,ws,t = setup(*SHAPES[name],None,XCHG)
     f=lambda: nat.check(lib.ff_chain_launch(ctypes.byref(ch),ctypes.byref(kc),ctypes.byref(t),ws.data_ptr(),ws.numel(),None))
     buf = torch.zeros(kc.grid_ctas*ST + 64, dtype=torch.int64, device='cuda')
     for _ in range(3): f()

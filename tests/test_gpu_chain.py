@@ -350,3 +350,29 @@ def test_fp16_chain_matches_oracle(case, exchange):
     ref = oracle.dense_chain(kind, act, host)
     assert np.isfinite(got).all()
     assert oracle.max_relative_error(got, ref_h) <= TOL and oracle.max_relative_error(got, ref) <= TOL
+
+
+@pytest.mark.parametrize("exchange", ["dsm", "l2"])
+@pytest.mark.parametrize("case", [("standard_ffn", "gelu", 512, 3072, 768, 768), ("gated_ffn", "silu", 256, 1024, 512, 512)],
+                         ids=["gpt2s", "gated-small"])
+def test_one_cta_region_finish_matches_oracle_and_repeats_bitwise(case, exchange):
+    """1-CTA kernels' opt-in split-N reduce-scatter through exchange regions (debug bit 29)."""
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = runtime.lower(graph, None, 148, exchange)
+    assert cfg.n_splits > 1
+    host, dev = _inputs(kind, m, n, k, l, seed=12)
+    lib = nat.load()
+    lib.ff_set_debug_mode(1 << 29)
+    try:
+        out1 = runtime.launch(graph, cfg, dev).clone()
+        out2 = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+    finally:
+        lib.ff_set_debug_mode(0)
+    _check(kind, act, host, out1)
+    assert torch.equal(out1, out2)
