@@ -213,7 +213,6 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   return w;
 }
 
-std::atomic<uint32_t> g_epoch{0};
 unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
 uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
 
@@ -221,7 +220,7 @@ uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
 // with 8-row slices, and the slab flags of every E tile fit their region.
 bool pair_finish_regions(const ffChainDesc* ch, const ffKernelConfig* c, int rings) {
   return c->n_splits > 1 && c->n_splits <= 8 && c->units <= rings && 128 % c->n_splits == 0 &&
-         (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 <= (1u << 17);
+         (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 < (1u << 17);
 }
 
 // Helper pairs (pair kernel) on the SMs a split-N launch leaves idle: they take
@@ -356,7 +355,9 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.n_units = cfg->units;
   a.n_rings = rings;
   a.act = ch->activation;
-  a.epoch = g_epoch.fetch_add(1) + 1;
+  a.epoch = 0;
+  a.dev_epoch = reinterpret_cast<uint32_t*>(wsb + wl.f_off) + (kFlagBytes / 4 - 1);  // last flag-region word
+  a.exit_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off) + (kCntBytes / 4 - 1);    // last counter word
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
@@ -375,7 +376,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   // region path adds the partner loads
   a.finish_tma = S > 1 && S <= 8 && 128 % S == 0 && R % 8 == 0 && cfg->units <= rings && !conv2 &&
                  (size_t)128 * kLB * 4 <= (size_t)C::kOFF_OWN && (size_t)R * kLB * 2 <= (size_t)C::kCHUNK_BYTES &&
-                 (size_t)cfg->m_tiles * (L / kLB) * 16 <= (1u << 17) && (g_dbg & (1u << 29));
+                 (size_t)cfg->m_tiles * (L / kLB) * 16 < (1u << 17) && (g_dbg & (1u << 29));
   if (implicit || conv2) {
     a.conv_k1 = implicit ? conv->k1 : 0;
     a.conv_H = conv->h;
@@ -549,7 +550,9 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.n_units = cfg->units;
   a.n_rings = rings;
   a.act = ch->activation;
-  a.epoch = g_epoch.fetch_add(1) + 1;
+  a.epoch = 0;
+  a.dev_epoch = reinterpret_cast<uint32_t*>(wsb + wl.f_off) + (kFlagBytes / 4 - 1);  // last flag-region word
+  a.exit_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off) + (kCntBytes / 4 - 1);    // last counter word
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
   a.ws = reinterpret_cast<float*>(wsb + wl.e_off);
   a.flags = reinterpret_cast<uint32_t*>(wsb + wl.f_off);
@@ -883,7 +886,7 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   if (cfg.exchange != FF_XCHG_DSM &&
       (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes / 2)
     return fail(FF_ERR_UNSUPPORTED, "too many (unit, step, member) chunks for the flag region");
-  if (cfg.n_splits > 1 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / cfg.lb) * sizeof(uint32_t) > kCntBytes)
+  if (cfg.n_splits > 1 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / cfg.lb) * sizeof(uint32_t) >= kCntBytes)
     return fail(FF_ERR_UNSUPPORTED, "too many E tiles for the split arrival counters");
   if (ws && reinterpret_cast<uintptr_t>(ws) % 256) return fail(FF_ERR_ARG, "workspace must be 256-byte aligned");
   LaunchFn fn = select_kernel(gated, cfg.nb, cfg.lb, cfg.exchange);

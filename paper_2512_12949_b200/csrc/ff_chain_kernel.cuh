@@ -57,7 +57,9 @@ struct ChainArgs {
   int n_units;         // m_tiles * l_clusters * S
   int n_rings;         // rings launched (persistent)
   int act;
-  uint32_t epoch;      // L2 mode: flag value of this launch (monotonic)
+  uint32_t epoch;      // unused (host-side epoch of earlier versions; see dev_epoch)
+  uint32_t* dev_epoch; // workspace word: epoch of the last completed launch; this launch's flags use +1
+  uint32_t* exit_cnt;  // workspace word (zero between launches): CTAs done; the last one advances dev_epoch
   __nv_bfloat16* E;    // output (S == 1)
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
@@ -140,6 +142,23 @@ __device__ __forceinline__ void apply_act_frag(int act, float (&v)[N]) {
   } else if (act == ACT_GELU_TANH) {
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = apply_act(ACT_GELU_TANH, v[i]);
+  }
+}
+
+// Launch epoch, kept on the device so that a launch captured in a CUDA graph
+// gets a fresh epoch on every replay (a host-side epoch would be frozen into the
+// graph and make the previous replay's ready flags look current).  Thread 0 of
+// every CTA reads the previous launch's epoch before the setup barrier; after
+// it, one idle thread counts the CTA in, and the last CTA to be counted (every
+// CTA has read by then) publishes this launch's epoch -- off the critical path.
+// Stream order keeps launches disjoint.
+__device__ __forceinline__ uint32_t epoch_begin(const ChainArgs& args) {
+  return ld_relaxed_gpu_u32(args.dev_epoch) + 1u;
+}
+__device__ __forceinline__ void epoch_publish(const ChainArgs& args, uint32_t epoch) {
+  if (atom_add_acqrel_gpu_u32(args.exit_cnt, 1u) == gridDim.x * gridDim.y * gridDim.z - 1u) {
+    *reinterpret_cast<volatile uint32_t*>(args.dev_epoch) = epoch;
+    *reinterpret_cast<volatile uint32_t*>(args.exit_cnt) = 0u;
   }
 }
 
@@ -257,6 +276,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
+  // the previous launch's epoch, loaded first so its latency hides behind the setup
+  const uint32_t epoch0 = threadIdx.x == 0 ? epoch_begin(args) : 0u;
   if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;
@@ -333,6 +354,8 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
   if (warp == 1) tmem_alloc<C::kTMEM_COLS>(tmem_slot);
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = epoch0;
   tc_fence_before();
   if (kDSM)
     cluster_sync();  // peers push into our buffers only after our barriers exist
@@ -340,6 +363,8 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+  const uint32_t epoch = s_epoch;
+  if (threadIdx.x == 96) epoch_publish(args, epoch);  // warp 3 lane 0: DSM recycler / idle
   if (threadIdx.x == 0) FF_STAMP(17);
 
   // slot h of global step T holds GEMM0 k-blocks [h*KB/G, (h+1)*KB/G) of step T+1
@@ -399,7 +424,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int tile = lo / C::BM; tile <= hi / C::BM; ++tile) {
             const uint32_t* f = args.flags + tile;  // unit id == m tile (ring 1, one step, one l cluster)
             uint32_t polls = 0;
-            FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+            FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - epoch) < 0) {
               if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
             });
           }
@@ -427,7 +452,7 @@ __global__ void __launch_bounds__(256, 1)
           // wait until ring member `origin` published chunk (unit, t)
           const uint32_t* f = flag_addr(u, t, origin);
           uint32_t polls = 0;
-          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - args.epoch) < 0) {
+          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - epoch) < 0) {
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
           });
           fence_proxy_async_global();
@@ -668,7 +693,7 @@ __global__ void __launch_bounds__(256, 1)
           bulk_commit();
           bulk_wait0();
           fence_proxy_async_global();
-          st_release_gpu_u32(flag_addr(u, t, (int)p), args.epoch);
+          st_release_gpu_u32(flag_addr(u, t, (int)p), epoch);
           mbar_arrive(own_free);
         }
       }
@@ -740,11 +765,11 @@ __global__ void __launch_bounds__(256, 1)
           if (issuer) FF_STAMP(24);
           uint32_t* const flags = args.flags + (1u << 17) + tile * 16;
           if (issuer) {
-            st_release_gpu_u32(flags + sp, args.epoch);
+            st_release_gpu_u32(flags + sp, epoch);
             uint32_t polls = 0;
             for (int j = 0; j < S; ++j) {
               if (j == sp) continue;
-              while ((int)(ld_relaxed_gpu_u32(flags + j) - args.epoch) < 0)
+              while ((int)(ld_relaxed_gpu_u32(flags + j) - epoch) < 0)
                 if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
             }
             fence_acq_rel_gpu();

@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t base = (raw_base + 1023u) & ~1023u;
   uint8_t* const smem_gen = smem_raw + (base - raw_base);
 
+  // the previous launch's epoch, loaded first so its latency hides behind the setup
+  const uint32_t epoch0 = threadIdx.x == 0 ? epoch_begin(args) : 0u;
   const int warp = threadIdx.x / 32;
   const int G = args.G;                  // ring members (pairs)
   const uint32_t crank = cluster_rank();
@@ -168,10 +170,14 @@ __global__ void __launch_bounds__(256, 1)
     if (G > 1 || !C::kOwnFull) tma_prefetch_desc(&maps.c);
   }
   if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = epoch0;
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(smem_gen + (tmem_slot - base));
+  const uint32_t epoch = s_epoch;
+  if (threadIdx.x == 96) epoch_publish(args, epoch);  // warp 3 lane 0 (idle warp)
   if (threadIdx.x == 0) FF_STAMP(17);
 
   // GEMM0 of step T+1 is spread over the first G - defer hops of step T; the
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(256, 1)
                 uint32_t v[8];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                  v[j] = args.epoch;
+                  v[j] = epoch;
                   if (h0 + j < nh && !((ready >> (h0 + j)) & 1ull)) {
                     Unit u;
                     int origin;
@@ -273,7 +279,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                  if (h0 + j < nh && (int)(v[j] - args.epoch) >= 0) ready |= 1ull << (h0 + j);
+                  if (h0 + j < nh && (int)(v[j] - epoch) >= 0) ready |= 1ull << (h0 + j);
               }
               if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
             }
@@ -478,10 +484,10 @@ __global__ void __launch_bounds__(256, 1)
               for (int j = 0; j < 8; ++j)  // independent loads: in flight together
                 v[j] = (o0 + j < G && !((ready >> (o0 + j)) & 1ull))
                            ? ld_relaxed_gpu_u32(flag_addr(u, t, o0 + j, (int)q))
-                           : args.epoch - 1u;
+                           : epoch - 1u;
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                if ((int)(v[j] - args.epoch) >= 0) ready |= 1ull << (o0 + j);
+                if ((int)(v[j] - epoch) >= 0) ready |= 1ull << (o0 + j);
             }
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
           } while (!((ready >> origin) & 1ull)));
@@ -683,7 +689,7 @@ __global__ void __launch_bounds__(256, 1)
       if (publish && issuer) {
         bulk_wait0();
         fence_proxy_async_global();
-        st_release_gpu_u32(flag_addr(u, t, p, (int)q), args.epoch);
+        st_release_gpu_u32(flag_addr(u, t, p, (int)q), epoch);
         mbar_arrive(own_free);
       }
       if (args.prof) t_store += clock64() - t_s0;
@@ -878,12 +884,12 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (issuer) {
       FF_STAMP(24);
-      st_release_gpu_u32(slab_flag(sp), args.epoch);
+      st_release_gpu_u32(slab_flag(sp), epoch);
       if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 25] = globaltimer_ns();
       uint32_t polls = 0;
       for (int j = 0; j < S; ++j) {
         if (j == sp) continue;
-        while ((int)(ld_relaxed_gpu_u32(slab_flag(j)) - args.epoch) < 0)
+        while ((int)(ld_relaxed_gpu_u32(slab_flag(j)) - epoch) < 0)
           if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
       }
       if (hx > 0)  // every helper segment (one per n-step) of this tile is in its region

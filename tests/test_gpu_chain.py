@@ -376,3 +376,33 @@ def test_one_cta_region_finish_matches_oracle_and_repeats_bitwise(case, exchange
         lib.ff_set_debug_mode(0)
     _check(kind, act, host, out1)
     assert torch.equal(out1, out2)
+
+
+@pytest.mark.parametrize("exchange", ["pair", "l2", "dsm"])
+def test_cuda_graph_capture_replays_the_chain(exchange):
+    """Stream capture of runtime.launch (no host sync, caller-owned workspace per
+    stream).  Every replay must see a fresh launch epoch (kept on the device): the
+    inputs change between replays, so a stale ready flag would leak the previous
+    replay's intermediate into the result."""
+    torch = _torch()
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = ("gated_ffn", "silu", 512, 8192, 2048, 2048)
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = runtime.lower(graph, None, 148, exchange)
+    host, dev = _inputs(kind, m, n, k, l, seed=21)
+    out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
+    a_static = dev["A"]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        runtime.launch(graph, cfg, dev, out=out, stream=st)  # workspace for this stream exists before capture
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            runtime.launch(graph, cfg, dev, out=out, stream=st)
+        for seed in (31, 32, 33):
+            new_a = oracle.round_bf16(oracle.make_inputs(kind, m, n, k, l, seed=seed)["A"])
+            a_static.copy_(torch.from_numpy(new_a).to(torch.bfloat16))
+            g.replay()
+            st.synchronize()
+            _check(kind, act, dict(host, A=new_a), out)
