@@ -161,3 +161,25 @@ def test_conv_block_matches_oracle(case):
         err_b, err = oracle.max_relative_error(got, ref_b), oracle.max_relative_error(got, ref)
         assert np.isfinite(got).all()
         assert err_b <= TOL and err <= TOL, (name, kcfg.as_dict(), err_b, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [("C5", (64, 56, 56, 64, 256, 3, 1), 1), ("block-3x3", (256, 14, 14, 64, 64, 1, 3), 2)],
+                         ids=lambda c: c[0])
+def test_conv_chain_fp16(case):
+    """fp16 storage through the implicit-GEMM conv paths (im2col TMA maps of FLOAT16)."""
+    import torch
+
+    from paper_2512_12949_b200 import runtime, workload as W
+
+    name, shape, batch = case
+    ic, h, w, oc1, oc2, k1, k2 = shape
+    cfg = W.ConvChainConfig(*shape) if k2 == 1 else W.ConvBlockConfig(*shape)
+    x, w1, w2 = (oracle.round_f16(a) for a in _conv_inputs(ic, h, w, oc1, oc2, k1, batch, seed=13, k2=k2))
+    dev = [torch.from_numpy(a).cuda().to(torch.float16).contiguous() for a in (x, w1, w2)]
+    y = runtime.run_conv(cfg, *dev, exchange="l2")
+    torch.cuda.synchronize()
+    assert y.dtype == torch.float16
+    got = y.float().cpu().numpy()
+    ref = oracle.conv_chain(x, w1, w2, "relu")
+    assert np.isfinite(got).all() and oracle.max_relative_error(got, ref) <= TOL
