@@ -44,6 +44,14 @@ int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tme
  * stream busy without touching memory, so a following launch sees a warm L2). */
 int ff_spin(long long cycles, int ctas, void* stream);
 
+/* DSM communication primitives (paper SIII-B dsm_comm; csrc/dsm_primitives.cuh) on one
+ * fp32 tile of `floats_per_cta` per CTA, `clusters` clusters of `cluster` CTAs, `iters`
+ * back-to-back repetitions (ms_out: event time of the launch).  op: 0 reduce-scatter
+ * (Add), 1 all-gather, 2 all-exchange (Add), 3 all-exchange (Mul: silu(gate) * up over
+ * CTA pairs), 4 one shuffle-ring hop.  in / out: device [cluster*clusters][floats_per_cta]. */
+int ff_dsm_primitive_run(int op, int cluster, int floats_per_cta, int clusters, const float* in, float* out,
+                         int iters, float* ms_out);
+
 const char* ff_dsm_last_error(void);
 
 #ifdef __cplusplus

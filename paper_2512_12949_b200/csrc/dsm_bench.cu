@@ -115,6 +115,11 @@ __global__ void spin_kernel(long long cycles) {
 
 }  // namespace
 
+namespace ff {
+// shared by the DSM primitive driver (dsm_primitives.cu): ff_dsm_last_error reports it
+void dsm_set_error(const char* msg) { g_err = msg; }
+}  // namespace ff
+
 extern "C" {
 
 const char* ff_dsm_last_error(void) { return g_err.c_str(); }
