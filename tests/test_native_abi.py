@@ -135,3 +135,22 @@ def test_workspace_sizes(lib):
             assert need >= 512 * 4096 * 4
         if exchange != "dsm" and cfg.ring > 1:
             assert need >= 512 * 16384 * 2
+
+
+def test_launch_argument_errors_without_touching_the_gpu(lib):
+    """ff_chain_launch rejects bad arguments before any CUDA work (FF_ERR_ARG = 5)."""
+    graph = W.build_standard_ffn(W.DimensionSpec(256, 1024, 256, 1024, 2), "relu")
+    cfg = runtime.lower(graph, None, 148, "l2")
+    ch = runtime.chain_desc(graph)
+    need = lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(cfg))
+    assert need > 0
+    null = nat.Tensors(None, None, None, None, None)
+    assert lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(null), None, 0, None) == 5
+    odd = nat.Tensors(0x1000 + 8, 0x2000, None, 0x3000, 0x4000)  # A not 16-byte aligned
+    assert lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(odd), 0x100000, need, None) == 5
+    ok = nat.Tensors(0x1000, 0x2000, None, 0x3000, 0x4000)
+    assert lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(ok), 0x100000, need - 1, None) == 5
+    assert b"workspace" in lib.ff_last_error()
+    bad_dtype = runtime.chain_desc(graph)
+    bad_dtype.dtype = 7
+    assert lib.ff_chain_launch(ctypes.byref(bad_dtype), ctypes.byref(cfg), ctypes.byref(ok), 0x100000, need, None) == 5
