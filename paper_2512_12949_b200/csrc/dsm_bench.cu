@@ -107,6 +107,57 @@ __global__ void __launch_bounds__(256, 1) launch_probe_big_kernel(const __grid_c
   }
 }
 
+// launch-latency probe with a chain kernel's register footprint (~170 registers per thread)
+__global__ void __launch_bounds__(256, 1) launch_probe_regs_kernel(unsigned long long* stamps, int n) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x] = t;
+  float v[160];
+#pragma unroll
+  for (int i = 0; i < 160; ++i) v[i] = (float)(i * n + threadIdx.x);
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int i = 0; i < 160; ++i) acc = fmaf(acc, v[(i + r) % 160], v[i]);
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x + 1] = t + (acc == 12345.f ? 1 : 0);
+}
+
+// launch-latency probe with eleven __grid_constant__ tensor maps (the pair kernel's params)
+struct ElevenMaps {
+  CUtensorMap m[11];
+};
+__global__ void __launch_bounds__(256, 1) launch_probe_tmap_kernel(const __grid_constant__ ElevenMaps maps,
+                                                                   unsigned long long* stamps, int prefetch) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x] = t;
+  if (prefetch && threadIdx.x == 0)
+    for (int i = 0; i < 11; ++i) ff::tma_prefetch_desc(&maps.m[i]);
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x + 1] = t;
+}
+
+// launch-latency probe with ~100 KB of (never executed) code
+__global__ void __launch_bounds__(256, 1) launch_probe_big_code_kernel(unsigned long long* stamps, int n, float* sink) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x] = t;
+  if (n == 12345) {  // never true at run time; the code is still in the binary
+    float a = sink[threadIdx.x], b = sink[threadIdx.x + 1];
+#pragma unroll
+    for (int i = 0; i < 3000; ++i) {
+      a = fmaf(a, b, (float)i);
+      b = fmaf(b, a, (float)(i ^ 7));
+      if ((i & 63) == 0) sink[threadIdx.x + i] = a;
+    }
+    sink[threadIdx.x] = a + b;
+  }
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) stamps[2 * blockIdx.x + 1] = t;
+}
+
 __global__ void spin_kernel(long long cycles) {
   const long long t0 = clock64();
   while (clock64() - t0 < cycles) {
@@ -209,7 +260,46 @@ int ff_launch_probe(void* stamps, int ctas, int smem_bytes, int cluster, int tme
   lc.attrs = a;
   lc.numAttrs = cluster > 1 ? 1 : 0;
   cudaError_t e;
-  if (tmem == 2) {
+  if (tmem == 6) {
+    static bool attr6 = false;
+    if (!attr6) {
+      cudaFuncSetAttribute(launch_probe_big_code_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+      cudaFuncSetAttribute(launch_probe_big_code_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr6 = true;
+    }
+    e = cudaLaunchKernelEx(&lc, launch_probe_big_code_kernel, reinterpret_cast<unsigned long long*>(stamps), 0,
+                           reinterpret_cast<float*>(stamps));
+  } else if (tmem == 4 || tmem == 5) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    ElevenMaps maps;
+    cuuint64_t dims[2] = {64, 256}, str[1] = {128};
+    cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+    for (int i = 0; i < 11; ++i)
+      reinterpret_cast<EncodeFn>(fp)(&maps.m[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, stamps, dims, str, box, es,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    static bool attr4 = false;
+    if (!attr4) {
+      cudaFuncSetAttribute(launch_probe_tmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+      cudaFuncSetAttribute(launch_probe_tmap_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr4 = true;
+    }
+    e = cudaLaunchKernelEx(&lc, launch_probe_tmap_kernel, maps, reinterpret_cast<unsigned long long*>(stamps),
+                           tmem == 5 ? 1 : 0);
+  } else if (tmem == 3) {
+    static bool attr3 = false;
+    if (!attr3) {
+      cudaFuncSetAttribute(launch_probe_regs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+      cudaFuncSetAttribute(launch_probe_regs_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      attr3 = true;
+    }
+    e = cudaLaunchKernelEx(&lc, launch_probe_regs_kernel, reinterpret_cast<unsigned long long*>(stamps), 3);
+  } else if (tmem == 2) {
     BigParams bp = {};
     lc.dynamicSmemBytes = 0;
     e = cudaLaunchKernelEx(&lc, launch_probe_big_kernel, bp, reinterpret_cast<unsigned long long*>(stamps));

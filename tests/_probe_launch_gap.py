@@ -57,8 +57,8 @@ for it in range(8):
     res.append((stamps[1].item()-stamps[0].item())/1e3)
 print(f"stamp->stamp {sorted(res)[4]:.1f} us")
 # launch-shape probe: empty kernel with the chain kernels' launch shape
-pst = torch.zeros(2 * 148, dtype=torch.int64, device='cuda')
-for ctas, smem, cl, tm in [(128,0,1,2),(128,0,2,2),(1,0,1,0),(128,0,1,0),(128,200*1024,1,0),(128,0,2,0),(128,200*1024,2,0),(128,200*1024,2,1),
+pst = torch.zeros(4096, dtype=torch.int64, device='cuda')
+for ctas, smem, cl, tm in [(128,200*1024,2,6),(128,0,1,6),(128,200*1024,2,4),(128,200*1024,2,5),(128,200*1024,2,3),(128,0,1,3),(128,0,1,2),(128,0,2,2),(1,0,1,0),(128,0,1,0),(128,200*1024,1,0),(128,0,2,0),(128,200*1024,2,0),(128,200*1024,2,1),
                            (128,220*1024,4,1),(148,220*1024,2,1),(96,200*1024,3,1)]:
     res=[]
     for it in range(8):
