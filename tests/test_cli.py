@@ -56,3 +56,30 @@ def test_simulate_runs_the_fused_kernel_and_verifies(capsys, tmp_path):
     assert doc["verify"]["max_rel_error"] <= 1e-2
     rc, doc = _run(capsys, ["run", "--dims", "512,8192,2048,2048", "--gated", "--iters", "5"])
     assert rc == 0 and doc["tflops"] > 100 and doc["exchange"] in ("pair", "l2", "dsm")
+
+
+def test_export_dot_plan_and_launch(capsys, tmp_path):
+    out = tmp_path / "top.json"
+    assert cli.main(["search", "--dims", "256,1024,256,512", "--activation", "relu", "--device", "b200",
+                     "--no-simulator-refine", "--top-k", "1", "--out", str(out)]) == 0
+    capsys.readouterr()
+    assert cli.main(["export-dot", "--dims", "256,1024,256,512", "--activation", "relu", "--plan", f"{out}#0"]) == 0
+    dot = capsys.readouterr().out
+    assert dot.startswith("digraph") and dot.rstrip().endswith("}") and dot.count("{") == dot.count("}")
+    assert "cta_0_0_0" in dot and "->" in dot
+    assert cli.main(["export-dot", "--dims", "512,8192,2048,2048", "--gated", "--launch", "pair"]) == 0
+    dot = capsys.readouterr().out
+    assert "CTA pair 0" in dot and "split-N reduce" in dot
+    assert cli.main(["export-dot", "--dims", "512,8192,2048,2048", "--gated"]) == 2  # needs --plan or --launch
+
+
+def test_export_tilegraph_cluster_structure():
+    from paper_2512_12949_b200 import tilegraph, workload as W
+    from paper_2512_12949_b200.plan import make_plan
+
+    g = W.build_gated_ffn(W.DimensionSpec(512, 8192, 2048, 2048))
+    p = make_plan("n", "klm", (64, 1024, 2048, 512), (1, 8, 2, 4), "spatial_split")
+    dot = tilegraph.export_tilegraph(g, p)
+    assert dot.count("[label=\"CTA (") == 16                       # cls_m * cls_n * cls_k
+    assert dot.count("all_exchange Mul") == 8 * 2                 # the two branch CTAs of each (im, in)
+    assert dot.count("shuffle") == 2 * 8                          # cls_shuffle = 2: rings of 2 per (ik, set)
