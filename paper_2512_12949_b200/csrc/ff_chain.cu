@@ -239,6 +239,7 @@ void plan_helpers(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   static const bool env_on = std::getenv("FF_HELPERS") != nullptr;
   if (c->exchange != FF_XCHG_L2_PAIR || (g_dbg & (1u << 24)) || !(env_on || (g_dbg & (1u << 26)))) return;
   if (!pair_finish_regions(ch, c, c->rings) || c->steps > 2 || c->l_clusters != 1) return;
+  if (ch->n != (int64_t)c->n_splits * c->steps * c->ring * c->nb) return;  // ragged n-steps
   const int H = (num_sms - c->rings * c->ring * 2) / 2;
   if (H < 1) return;
   const double r = (double)ch->k / (ch->kind == FF_KIND_GATED ? 128 : 256);
@@ -545,6 +546,8 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.G = cfg->ring;
   a.S = cfg->n_splits;
   a.steps = cfg->steps;
+  a.total_chunks = (int)(N / C::kN0);
+  a.split_chunks = (a.total_chunks + cfg->n_splits - 1) / cfg->n_splits;
   a.m_tiles = cfg->m_tiles;
   a.l_clusters = cfg->l_clusters;
   a.n_units = cfg->units;
@@ -644,6 +647,18 @@ int launch_pair_dispatch(const ffChainDesc* ch, const ffKernelConfig* cfg, const
 using LaunchFn = int (*)(const ffChainDesc*, const ffKernelConfig*, const ffTensors*, void*, void*, cudaStream_t,
                          const ffConvDesc*);
 
+// Can N be cut into S splits of this config's chunks?  The 1-CTA kernels need
+// whole n-steps in equal splits; the pair kernel takes ceil(chunks / S) chunks
+// per split and a ragged last n-step (the last split shorter), as long as
+// every split keeps at least one chunk.
+bool splits_ok(const ffChainDesc* ch, const ffKernelConfig* c, int64_t S) {
+  if (S < 1) return false;
+  if (c->exchange != FF_XCHG_L2_PAIR) return ch->n % (S * c->ring * c->nb) == 0;
+  if (ch->n % c->nb) return false;
+  const int64_t chunks = ch->n / c->nb, per = (chunks + S - 1) / S;
+  return chunks - (S - 1) * per >= 1;
+}
+
 LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
   if (mode == FF_XCHG_L2_PAIR) {
     if (nb != (gated ? 128 : 256) || lb != 256) return nullptr;
@@ -696,10 +711,15 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
     return fail(FF_ERR_UNSUPPORTED, "pair kernel needs k % 128 == 0 and 256-column E slices");
   const int64_t lcover = (int64_t)c->ring * c->lb;
   if (ch->l % lcover) return fail(FF_ERR_UNSUPPORTED, "ring * lb must divide l");
-  const int64_t nstep = (int64_t)c->n_splits * c->ring * c->nb;
-  if (ch->n % nstep) return fail(FF_ERR_UNSUPPORTED, "n_splits * ring * nb must divide n");
+  if (!splits_ok(ch, c, c->n_splits))
+    return fail(FF_ERR_UNSUPPORTED, c->exchange == FF_XCHG_L2_PAIR
+                                        ? "nb must divide n and every N split must keep a chunk"
+                                        : "n_splits * ring * nb must divide n");
   c->l_clusters = (int32_t)(ch->l / lcover);
-  c->steps = (int32_t)(ch->n / nstep);
+  {  // pair kernel: ceil(chunks / S) chunks per split, the last n-step possibly ragged
+    const int64_t per = (ch->n / c->nb + c->n_splits - 1) / c->n_splits;
+    c->steps = (int32_t)((per + c->ring - 1) / c->ring);
+  }
   const int rows = 128 * width;
   c->m_tiles = (int32_t)((ch->m + rows - 1) / rows);
   const int64_t units = (int64_t)c->m_tiles * c->l_clusters * c->n_splits;
@@ -728,7 +748,7 @@ void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
     const int64_t per = (int64_t)((ch->m + 128 * width - 1) / (128 * width)) * (ch->l / ((int64_t)c->ring * c->lb));
     const int64_t next = (int64_t)c->n_splits * 2;
     if (per * next > max_rings) break;
-    if (ch->n % (next * c->ring * c->nb)) break;
+    if (!splits_ok(ch, c, next)) break;
     c->n_splits = (int32_t)next;
   }
 }
@@ -768,7 +788,7 @@ int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, 
     for (int64_t ring = std::min<int64_t>(slices, max_ring); ring >= 1 && !c.lb; --ring) {
       if (slices % ring) continue;
       for (int nb : nb_opts)
-        if (nb && ch->n % (ring * nb) == 0) {
+        if (nb && ch->n % ((pair ? 1 : ring) * nb) == 0) {
           c.lb = lb;
           c.ring = (int32_t)ring;
           c.nb = nb;
@@ -838,10 +858,9 @@ int ff_plan_lower_ex(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_
   const int32_t reduce_sets = (cn * ck) / cl;
   c.n_splits = (int32_t)(grid_n * reduce_sets);
   c.nb = exchange == FF_XCHG_L2_PAIR ? (gated ? 128 : 256) : (gated ? 64 : 128);
-  while (c.n_splits > 1 && ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.n_splits /= 2;
-  if (exchange != FF_XCHG_L2_PAIR && ch->n % ((int64_t)c.n_splits * c.ring * c.nb)) c.nb = 64;
-  if (ch->n % ((int64_t)c.n_splits * c.ring * c.nb))
-    return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");
+  while (c.n_splits > 1 && !splits_ok(ch, &c, c.n_splits)) c.n_splits /= 2;
+  if (!splits_ok(ch, &c, c.n_splits) && exchange != FF_XCHG_L2_PAIR) c.nb = 64;
+  if (!splits_ok(ch, &c, c.n_splits)) return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");
   fill_machine(ch, &c, num_sms);
   rc = finish_config(ch, &c, num_sms);
   if (rc) return rc;

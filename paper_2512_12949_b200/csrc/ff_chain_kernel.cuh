@@ -52,6 +52,8 @@ struct ChainArgs {
   int G;               // ring size
   int S;               // N splits
   int steps;           // n-steps per split
+  int split_chunks;    // pair kernel: C chunks (kN0 columns) per N split, ceil(total / n_splits)
+  int total_chunks;    // pair kernel: N / kN0 (the last split and its last n-step may be ragged)
   int m_tiles;         // ceil(M / 128)
   int l_clusters;      // L / (G * LB)
   int n_units;         // m_tiles * l_clusters * S

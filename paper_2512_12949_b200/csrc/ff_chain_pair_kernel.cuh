@@ -133,7 +133,16 @@ __global__ void __launch_bounds__(256, 1)
     const int rest = u / args.m_tiles;
     const int lc = rest % args.l_clusters;
     const int split = rest / args.l_clusters;
-    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * steps * G * C::kN0, u, split};
+    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * args.split_chunks * C::kN0, u, split};
+  };
+  // ragged n-steps: split s owns chunks [s * split_chunks, min(N / kN0, (s + 1) * split_chunks)),
+  // chunk t * G + origin of a split is GEMM0'd by member `origin` in n-step t.  A member
+  // without a chunk keeps every barrier handshake (empty GEMM0 commits, drain-less
+  // arrivals) and skips the work.  T is the member's global step index.
+  auto has_chunk = [&](int T, int origin) {
+    const int split = unit_of(T / steps).split;
+    const int lim = min(args.split_chunks, args.total_chunks - split * args.split_chunks);
+    return (T % steps) * G + origin < lim;
   };
 
   const uint32_t bar0 = base + C::kOFF_BAR;
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(256, 1)
       return Seg{t, mp % args.m_tiles, mp / args.m_tiles};
     };
     auto unit_at = [&](const Seg& g, int split) {  // l_clusters == 1
-      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * steps * G * C::kN0, g.mt + args.m_tiles * split, split};
+      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * args.split_chunks * C::kN0, g.mt + args.m_tiles * split, split};
     };
     // E buffer eb's barriers (selects, not a local array: a dynamically indexed
     // array would give the kernel a stack frame)
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(256, 1)
         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
       };
       auto load_gemm0 = [&](int T, int kb0, int kb1) {
-        if (kb0 >= kb1) return;
+        if (kb0 >= kb1 || !has_chunk(T, p)) return;
         const Unit u = unit_of(T / steps);
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
         const int nblk = (u.n0 + ((T % steps) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
@@ -474,6 +483,7 @@ __global__ void __launch_bounds__(256, 1)
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
         if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
+        if (!has_chunk(T, origin)) return;  // ragged n-step: no chunk from this origin
         if (from_l2 && !((ready >> origin) & 1ull) && !(args.dbg & 2u)) {
           // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
@@ -545,7 +555,8 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, (T & 1) ^ 1));
           tc_fence_after();
         }
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const bool has = has_chunk(T, p);
+        for (int kb = kb0; kb < (has ? kb1 : kb0); ++kb) {
           FF_TIMED(w_full0, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
@@ -579,7 +590,8 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (C::kOwnFull && h == 0) FF_TIMED(w_own, mbar_wait_cluster(own_full, T & 1));
         tc_fence_after();
-        for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
+        const bool has = has_chunk(T, (p - h + G) % G);
+        for (int kb2 = 0; kb2 < (has ? C::kCW / C::BK : 0); ++kb2) {
           FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
@@ -635,8 +647,14 @@ __global__ void __launch_bounds__(256, 1)
       const bool publish = G > 1 || !C::kOwnFull;  // the chunk goes to the L2 scratch
       const int nblk = (u.n0 + (t * G + p) * C::kN0) / 64;
       constexpr int kRoundCols = C::kOWN_BYTES / (C::BM * 2);  // 128 columns per own-slot round
+      const bool has = has_chunk(T, p);
+      if (!has) {  // ragged last n-step without a chunk here: the handshakes only
+        tc_fence_before();
+        mbar_arrive_remote(L_c_empty);
+        if (C::kOwnFull) mbar_arrive_remote(L_own_full);
+      }
 #pragma unroll 1
-      for (int r0 = 0; r0 < C::kCW; r0 += kRoundCols) {
+      for (int r0 = 0; r0 < (has ? C::kCW : 0); r0 += kRoundCols) {
         if (r0 > 0) {  // the previous round's TMA store must have read the own slot
           if (issuer) bulk_wait_read0();
           named_bar_sync(1, 128);
@@ -687,9 +705,11 @@ __global__ void __launch_bounds__(256, 1)
       if (issuer && T < 2) FF_STAMP(19 + 3 * T);
       const unsigned long long t_s0 = args.prof ? clock64() : 0ull;
       if (publish && issuer) {
-        bulk_wait0();
-        fence_proxy_async_global();
-        st_release_gpu_u32(flag_addr(u, t, p, (int)q), epoch);
+        if (has) {
+          bulk_wait0();
+          fence_proxy_async_global();
+          st_release_gpu_u32(flag_addr(u, t, p, (int)q), epoch);
+        }
         mbar_arrive(own_free);
       }
       if (args.prof) t_store += clock64() - t_s0;

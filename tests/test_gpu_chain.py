@@ -289,6 +289,48 @@ def test_random_shapes_match_oracle(case, exchange):
     _check(kind, act, host, out)
 
 
+# ragged n-steps of the pair kernel: ceil(chunks / S) chunks per N split, so the last
+# n-step (and the last split) may be short; `total` = N / nb chunks
+@pytest.mark.parametrize("kind,ring,splits,total", [("standard_ffn", 4, 1, 5), ("standard_ffn", 4, 2, 6),
+                                                    ("standard_ffn", 3, 2, 7), ("standard_ffn", 6, 1, 1),
+                                                    ("standard_ffn", 2, 4, 11), ("gated_ffn", 4, 2, 9),
+                                                    ("gated_ffn", 3, 4, 13)])
+def test_pair_ragged_steps_match_oracle(kind, ring, splits, total):
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    act = "silu" if kind == "gated_ffn" else "gelu"
+    nb = 128 if kind == "gated_ffn" else 256
+    m, k, lb = 384, 256, 256
+    l, n = ring * lb, total * nb
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = nat.KernelConfig()
+    cfg.ring, cfg.n_splits, cfg.nb, cfg.lb, cfg.exchange = ring, splits, nb, lb, runtime.EXCHANGES["pair"]
+    host, dev = _inputs(kind, m, n, k, l, seed=ring + 7 * total)
+    out1 = runtime.launch(graph, cfg, dev).clone()
+    out2 = runtime.launch(graph, cfg, dev)
+    torch.cuda.synchronize()
+    _check(kind, act, host, out1)
+    assert torch.equal(out1, out2)
+
+
+@pytest.mark.parametrize("case", [("gated_ffn", "silu", 512, 11008, 4096, 4096),     # LLaMA-7B (reference preset S3)
+                                  ("standard_ffn", "relu", 256, 8960, 1536, 1536)], ids=["llama7b", "ragged-std"])
+def test_auto_lowering_with_ragged_ring(case):
+    """Shapes whose chunks do not fill the widest ring lower to a ragged pair ring."""
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = runtime.lower(graph, None, 148, "pair")
+    assert n != cfg.n_splits * cfg.steps * cfg.ring * cfg.nb and cfg.l_clusters == 1
+    host, dev = _inputs(kind, m, n, k, l, seed=5)
+    out = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    _check(kind, act, host, out)
+
+
 def test_workspace_zero_invariant_across_configs():
     """The split counters and the fp32 E zone of the shared per-stream workspace
     are zero after every launch (configs reuse one workspace; a config whose

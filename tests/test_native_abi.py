@@ -62,7 +62,11 @@ def _check_cfg(graph, cfg):
     d = graph.dims
     width = 2 if cfg.exchange == nat.XCHG_L2_PAIR else 1
     assert d.l % (cfg.ring * cfg.lb) == 0
-    assert d.n % (cfg.n_splits * cfg.ring * cfg.nb) == 0
+    if cfg.exchange == nat.XCHG_L2_PAIR:  # ragged last n-step allowed
+        assert d.n % (cfg.n_splits * cfg.nb) == 0
+        assert cfg.steps == -(-d.n // (cfg.n_splits * cfg.ring * cfg.nb))
+    else:
+        assert d.n % (cfg.n_splits * cfg.ring * cfg.nb) == 0
     assert cfg.m_tiles == -(-d.m // (128 * width))
     assert cfg.units == cfg.m_tiles * cfg.l_clusters * cfg.n_splits
     assert 1 <= cfg.rings <= cfg.units
