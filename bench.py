@@ -344,6 +344,75 @@ def time_steps(fn, steps, flush, stream):
     return [a.elapsed_time(b) for a, b in evs]
 
 
+def e2e_pipelined(graph, cfg, tensors, host_a, kind, m, l, steps, dev):
+    """Serving-style end-to-end loop through the public API: every step uploads its
+    own A from pinned host memory and downloads its E, double-buffered so that step
+    i's upload (copy stream 1) and step i-1's download (copy stream 2) overlap step
+    i's chain on the compute stream.  Weights rotate over `n_sets` device copies
+    (working set > L2, so no flush kernel sits in the timed region).  Timed from one
+    event before the first upload to one after the last download."""
+    import torch
+
+    from paper_2512_12949_b200 import runtime
+
+    wbytes = sum(t.numel() * t.element_size() for n, t in tensors.items() if n != "A")
+    n_sets = min(16, max(4, -(-int(2.5 * 126e6) // wbytes)))
+    n_sets += n_sets & 1  # (set, buffer) pairs repeat with period n_sets: <= 16 tensor-map cache keys
+    sets = []
+    for j in range(n_sets):
+        w = {"D": tensors["D"].clone()}
+        if kind == "gated_ffn":
+            packed = torch.stack([tensors["B0"], tensors["B1"]])
+            w["B0"], w["B1"] = packed[0], packed[1]
+        else:
+            w["B"] = tensors["B"].clone()
+        sets.append(w)
+    hosts_a = [host_a, host_a.clone().pin_memory()]
+    hosts_e = [torch.empty((m, l), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    devs_a = [torch.empty_like(tensors["A"]) for _ in range(2)]
+    outs = [torch.empty((m, l), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    # three created streams: work on the legacy default stream would serialise with both copy streams
+    stream, s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(n):
+        k_done = [None] * n
+        o_done = [None] * n
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        s_in.wait_event(start)
+        s_out.wait_event(start)
+        for i in range(n):
+            b = i & 1
+            with torch.cuda.stream(s_in):  # A of step i; its buffer was last read by chain i-2
+                if i >= 2:
+                    s_in.wait_event(k_done[i - 2])
+                devs_a[b].copy_(hosts_a[b], non_blocking=True)
+                a_in = torch.cuda.Event()
+                a_in.record(s_in)
+            stream.wait_event(a_in)
+            if i >= 2:  # E buffer b was downloaded by step i-2
+                stream.wait_event(o_done[i - 2])
+            t = dict(sets[i % n_sets], A=devs_a[b])
+            runtime.launch(graph, cfg, t, out=outs[b], stream=stream)
+            k_done[i] = torch.cuda.Event()
+            k_done[i].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(k_done[i])
+                hosts_e[b].copy_(outs[b], non_blocking=True)
+                o_done[i] = torch.cuda.Event()
+                o_done[i].record(s_out)
+        stream.wait_event(o_done[n - 1])
+        end.record(stream)
+        torch.cuda.synchronize()
+        return start.elapsed_time(end)
+
+    run(4)
+    ms = run(steps)
+    return {"ms_total": ms, "schedule": f"pipelined: H2D of step i and D2H of step i-1 on two copy streams overlap "
+                                        f"chain i; weights rotate over {n_sets} device copies (> L2), no flush; "
+                                        f"one event pair around all {steps} steps"}
+
+
 def _max_over_ranks(x, dev):
     import torch
     import torch.distributed as dist
@@ -426,6 +495,11 @@ def run_ours(args, rank, world, local_rank):
         e2e_ms = _max_over_ranks(e2e_ms, dev)
     e2e_value = job_fl * args.steps / (e2e_ms * 1e-3) / 1e12
 
+    e2e_pipe = e2e_pipelined(graph, cfg, tensors, host_a, kind, m, l, args.steps, dev)
+    if world > 1:
+        e2e_pipe["ms_total"] = _max_over_ranks(e2e_pipe["ms_total"], dev)
+    e2e_pipe_value = job_fl * args.steps / (e2e_pipe["ms_total"] * 1e-3) / 1e12
+
     # unfused cuBLAS on the same config
     cub = cublas_unfused(kind, act, tensors, flush, stream, max(args.steps, 5))
 
@@ -459,9 +533,14 @@ def run_ours(args, rank, world, local_rank):
                      "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
                      "traffic": ncu.get("dram_bytes_per_launch"), "peak_source": peaks["source"],
                      "kernel_ms_median": round(kern_ms, 4)},
-        "e2e": {"value": round(e2e_value, 2), "unit": "TFLOP/s", "h2d_bytes_per_step": int(host_a.numel() * 2),
-                "d2h_bytes_per_step": int(host_e.numel() * 2), "ms_per_step": round(e2e_ms / args.steps, 4),
-                "api": "paper_2512_12949_b200.runtime.launch (C ABI ff_chain_launch)"},
+        "e2e": {"value": round(e2e_pipe_value, 2), "unit": "TFLOP/s", "h2d_bytes_per_step": int(host_a.numel() * 2),
+                "d2h_bytes_per_step": int(host_e.numel() * 2),
+                "ms_per_step": round(e2e_pipe["ms_total"] / args.steps, 4),
+                "api": "paper_2512_12949_b200.runtime.launch (C ABI ff_chain_launch)",
+                "schedule": e2e_pipe["schedule"],
+                "serial": {"value": round(e2e_value, 2), "ms_per_step": round(e2e_ms / args.steps, 4),
+                           "schedule": "one stream per step: H2D A, chain, D2H E, L2 flushed between steps "
+                                       "(outside the per-step events)"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "cublas_unfused": cub,

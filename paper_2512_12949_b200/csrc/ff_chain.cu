@@ -451,7 +451,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     ff::PairMaps maps;
     bool valid;
   };
-  thread_local Entry cache[4] = {};
+  thread_local Entry cache[16] = {};  // serving loops rotate buffers
   thread_local int cache_next = 0;
   ff::PairMaps maps;
   bool hit = false;
@@ -526,7 +526,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
       cache[cache_next].key = key;
       cache[cache_next].maps = maps;
       cache[cache_next].valid = true;
-      cache_next = (cache_next + 1) % 4;
+      cache_next = (cache_next + 1) % 16;
     }
   }
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
