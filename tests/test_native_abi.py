@@ -62,9 +62,12 @@ def _check_cfg(graph, cfg):
     d = graph.dims
     width = 2 if cfg.exchange == nat.XCHG_L2_PAIR else 1
     assert d.l % (cfg.ring * cfg.lb) == 0
-    if cfg.exchange == nat.XCHG_L2_PAIR:  # ragged last n-step allowed
-        assert d.n % (cfg.n_splits * cfg.nb) == 0
-        assert cfg.steps == -(-d.n // (cfg.n_splits * cfg.ring * cfg.nb))
+    if cfg.exchange == nat.XCHG_L2_PAIR:  # ceil(chunks / S) chunks per split, ragged last n-step
+        assert d.n % cfg.nb == 0
+        chunks = d.n // cfg.nb
+        per = -(-chunks // cfg.n_splits)
+        assert chunks - (cfg.n_splits - 1) * per >= 1
+        assert cfg.steps == -(-per // cfg.ring)
     else:
         assert d.n % (cfg.n_splits * cfg.ring * cfg.nb) == 0
     assert cfg.m_tiles == -(-d.m // (128 * width))
