@@ -405,13 +405,13 @@ struct PairStages {
   static constexpr int value = kMax > 4 ? 4 : kMax;
 };
 
-template <bool kGated, bool kPacked, bool kQuad>
+template <bool kGated, bool kPacked, bool kQuad, bool kRagged>
 int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
                      cudaStream_t stream, const ffConvDesc*) {
   constexpr int kStages = PairStages<kGated>::value;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
   using C = ff::PairCfg<kGated, 256, kStages>;
-  auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked, kQuad>;
+  auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked, kQuad, kRagged>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM); });
@@ -629,8 +629,11 @@ bool quad_ok(const ffKernelConfig* cfg) {
 template <bool kGated, bool kPacked>
 int launch_pair_q(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws, void* c_debug,
                   cudaStream_t stream, const ffConvDesc* conv) {
-  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true>(ch, cfg, t, ws, c_debug, stream, conv)
-                      : launch_pair_impl<kGated, kPacked, false>(ch, cfg, t, ws, c_debug, stream, conv);
+  // ragged n-steps (N not a whole number of ring steps per split): plain pairs only
+  if (ch->n != (int64_t)cfg->n_splits * cfg->steps * cfg->ring * cfg->nb)
+    return launch_pair_impl<kGated, kPacked, false, true>(ch, cfg, t, ws, c_debug, stream, conv);
+  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true, false>(ch, cfg, t, ws, c_debug, stream, conv)
+                      : launch_pair_impl<kGated, kPacked, false, false>(ch, cfg, t, ws, c_debug, stream, conv);
 }
 
 int launch_pair_dispatch(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,

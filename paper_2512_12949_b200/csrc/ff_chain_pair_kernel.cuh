@@ -74,7 +74,9 @@ struct PairCfg {
 // by both leaders' commits (empty-barrier count 2, commit mask 0xF).
 #undef FF_PROF_ROW
 #define FF_PROF_ROW vcta
-template <bool kGated, int kLB, int kStages, bool kPackedB, bool kQuad>
+// kRagged: N need not fill whole n-steps of every split (see has_chunk); a separate
+// instantiation so the common case keeps its exact code.
+template <bool kGated, int kLB, int kStages, bool kPackedB, bool kQuad, bool kRagged>
 __global__ void __launch_bounds__(256, 1)
     ff_chain_pair_kernel(const __grid_constant__ PairMaps maps, const ChainArgs args) {
   using C = PairCfg<kGated, kLB, kStages>;
@@ -133,13 +135,15 @@ __global__ void __launch_bounds__(256, 1)
     const int rest = u / args.m_tiles;
     const int lc = rest % args.l_clusters;
     const int split = rest / args.l_clusters;
-    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * args.split_chunks * C::kN0, u, split};
+    return Unit{mt * 2 * C::BM, (lc * G + p) * kLB, split * (kRagged ? args.split_chunks : steps * G) * C::kN0, u,
+                split};
   };
   // ragged n-steps: split s owns chunks [s * split_chunks, min(N / kN0, (s + 1) * split_chunks)),
   // chunk t * G + origin of a split is GEMM0'd by member `origin` in n-step t.  A member
   // without a chunk keeps every barrier handshake (empty GEMM0 commits, drain-less
   // arrivals) and skips the work.  T is the member's global step index.
   auto has_chunk = [&](int T, int origin) {
+    if (!kRagged) return true;
     const int split = unit_of(T / steps).split;
     const int lim = min(args.split_chunks, args.total_chunks - split * args.split_chunks);
     return (T % steps) * G + origin < lim;
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(256, 1)
       return Seg{t, mp % args.m_tiles, mp / args.m_tiles};
     };
     auto unit_at = [&](const Seg& g, int split) {  // l_clusters == 1
-      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * args.split_chunks * C::kN0, g.mt + args.m_tiles * split, split};
+      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * steps * G * C::kN0, g.mt + args.m_tiles * split, split};
     };
     // E buffer eb's barriers (selects, not a local array: a dynamically indexed
     // array would give the kernel a stack frame)
