@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t bx = bar0 + 8u * (2 * kStages);
   const uint32_t c_full = bx, c_empty = bx + 8, own_full = bx + 16, own_free = bx + 24;
   const uint32_t e_full = bx + 32, e_empty = bx + 40, e_load = bx + 48;
+  const uint32_t c_full1 = bx + 56;  // C(1) in E's columns (swap_e below): its own barrier, since
+                                     // c_full could complete twice before the epilogue looks
   const uint32_t tmem_slot = bar0 + 8u * C::kNUM_BARS;
   const uint32_t own_slot = base + C::kOFF_OWN;
   const uint16_t kPairMask = (uint16_t)(0x3u << lrank);
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(256, 1)
     mbar_init(e_full, 1);
     mbar_init(e_empty, 256);
     mbar_init(e_load, 1);
+    mbar_init(c_full1, 1);
     fence_mbar_init();
   }
   if (warp == 0 && elect_one()) {
@@ -203,6 +206,13 @@ __global__ void __launch_bounds__(256, 1)
     const int g0_slices = (Tn == total_steps - 1 && args.defer_last) ? 1 : G - args.defer;
     return h < g0_slices ? h * kblocks / g0_slices : kblocks;
   };
+  // One unit of two n-steps (the M=512 chains): GEMM0(1) runs before any hop of
+  // step 0, while the E accumulator is still unused, so it accumulates in E's TMEM
+  // columns instead of waiting for the epilogue to drain C(0); E then lives in the
+  // drained C columns.  Removes the C-drain bubble from the tensor pipe.
+  const bool swap_e = args.defer_last && total_steps == 2 && steps == 2 && hx == 0 && !(args.dbg & (1u << 30));
+  const uint32_t e_col = swap_e ? 0u : (uint32_t)C::kTMEM_E;
+  auto c_col = [&](int T) { return (swap_e && T == 1) ? (uint32_t)C::kTMEM_E : 0u; };
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
   };
@@ -555,10 +565,11 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t idesc1 = idesc_as(idesc_bf16(256, kLB, 0, 1), args.f16);
       auto gemm0 = [&](int T, int kb0, int kb1) {
         if (kb0 >= kb1) return;
-        if (kb0 == 0) {
+        if (kb0 == 0 && !(swap_e && T == 1)) {
           FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, (T & 1) ^ 1));
           tc_fence_after();
         }
+        const uint32_t cacc = tmem_base + c_col(T);
         const bool has = has_chunk(T, p);
         for (int kb = kb0; kb < (has ? kb1 : kb0); ++kb) {
           FF_TIMED(w_full0, mbar_wait(full_bar(stage), phase));
@@ -570,16 +581,16 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             if (args.dbg & 1u) continue;
             if (kGated) {
-              umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
-              umma_bf16_pair(tmem_base + C::kN0, ad, b_desc(sb + C::kSLOT + C::kSLOT / 2, kk), idesc0, acc);
+              umma_bf16_pair(cacc, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
+              umma_bf16_pair(cacc + C::kN0, ad, b_desc(sb + C::kSLOT + C::kSLOT / 2, kk), idesc0, acc);
             } else {
-              umma_bf16_pair(tmem_base, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
+              umma_bf16_pair(cacc, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
             }
           }
           umma_commit_pair(empty_bar(stage), kStageMask);
           next();
         }
-        if (kb1 == kblocks) umma_commit_pair(c_full, kPairMask);
+        if (kb1 == kblocks) umma_commit_pair((swap_e && T == 1) ? c_full1 : c_full, kPairMask);
       };
       bool e_started = false;
       auto hop = [&](int T, int h) {
@@ -592,6 +603,9 @@ __global__ void __launch_bounds__(256, 1)
           }
           e_started = false;
         }
+        if (swap_e && T == 0 && h == 0) {  // E goes to C(0)'s columns: drained?
+          FF_TIMED(w_cempty, mbar_wait_cluster(c_empty, 0));
+        }
         if (C::kOwnFull && h == 0) FF_TIMED(w_own, mbar_wait_cluster(own_full, T & 1));
         tc_fence_after();
         const bool has = has_chunk(T, (p - h + G) % G);
@@ -603,7 +617,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             if (!(args.dbg & 1u))
-              umma_bf16_pair(tmem_base + C::kTMEM_E, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
+              umma_bf16_pair(tmem_base + e_col, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
                              e_started ? 1u : 0u);
             e_started = true;
           }
@@ -643,7 +657,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int T = 0; T < total_steps; ++T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
-      FF_TIMED(w_cfull, mbar_wait_cluster(c_full, T & 1));
+      FF_TIMED(w_cfull, (swap_e && T == 1) ? mbar_wait_cluster(c_full1, 0) : mbar_wait_cluster(c_full, T & 1));
       tc_fence_after();
       if (issuer && T < 2) FF_STAMP(18 + 3 * T);
       FF_TIMED(w_ofree, mbar_wait_cluster(own_free, (T & 1) ^ 1));
@@ -668,11 +682,11 @@ __global__ void __launch_bounds__(256, 1)
           float v[32];
           if (kGated) {
             float w[32];
-            tmem_ld32x2(lane_base + c0, lane_base + C::kN0 + c0, v, w);
+            tmem_ld32x2(lane_base + c_col(T) + c0, lane_base + c_col(T) + C::kN0 + c0, v, w);
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = silu_fast(v[i]) * w[i];
           } else {
-            tmem_ld32(lane_base + c0, v);
+            tmem_ld32(lane_base + c_col(T) + c0, v);
             apply_act_frag(args.act, v);
           }
           uint32_t pk[16];
@@ -742,7 +756,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
           for (int c0 = 0; c0 < kLB; c0 += 32) {
             float v[32];
-            tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+            tmem_ld32(lane_base + e_col + c0, v);
             const uint32_t tile = base + (c0 / cols_per_tile) * 16384;
             if (bf16_out) {
               uint32_t pk[16];
@@ -786,7 +800,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
           for (int c0 = g0; c0 < g1; c0 += 32) {
             float v[32];
-            tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+            tmem_ld32(lane_base + e_col + c0, v);
             const uint32_t tile = stg + ((c0 - g0) / cols_per_tile) * 16384;
             if (bf16_out) {
               uint32_t pk[16];
@@ -882,7 +896,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
       for (int c0 = c_lo; c0 < c_lo + kLB / 2; c0 += 64) {
         float v[32], w[32];
-        tmem_ld32x2(lane_base + C::kTMEM_E + c0, lane_base + C::kTMEM_E + c0 + 32, v, w);
+        tmem_ld32x2(lane_base + e_col + c0, lane_base + e_col + c0 + 32, v, w);
         if (slice != sp) {  // another split's row: straight to this split's exchange region
 #pragma unroll
           for (int j = 0; j < 8; ++j) {

@@ -4,7 +4,10 @@ import sys
 import torch
 sys.path.insert(0, '.')
 import bench
-from paper_2512_12949_b200 import runtime
+import os
+from paper_2512_12949_b200 import _native as nat, runtime
+if os.environ.get('FF_DBG'):
+    nat.load().ff_set_debug_mode(int(os.environ['FF_DBG'], 0))
 dev = torch.device('cuda', 0)
 flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
 for name in sys.argv[1:]:
