@@ -17,7 +17,7 @@ for r in rows:
     unit = r["Metric Unit"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "us": 1e3, "ms": 1e6}.get(unit, 1)
     launches[-1]["m"][r["Metric Name"]] = v * scale if isinstance(v, float) else v
-doc = {"round": "r01 (session 2)", "method": "ncu --cache-control all --clock-control none --metrics gpu__time_duration.sum,"
+doc = {"round": "r01 (session 5)", "method": "ncu --cache-control all --clock-control none --metrics gpu__time_duration.sum,"
        "dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed "
        "python tests/_profile_run.py (FF_NO_COOPERATIVE=1); per-launch values are cold-cache and serialised"}
 i = 0
