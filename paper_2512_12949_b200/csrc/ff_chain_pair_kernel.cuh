@@ -946,60 +946,43 @@ __global__ void __launch_bounds__(256, 1)
     // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
     const uint8_t* const src = smem_gen;
     const int n_items = (args.dbg & 32u) ? 0 : R * kChunks;  // diagnostics: skip the sum
+    // R = 128 / S is a power of two (pair_finish_regions): item -> (chunk, row) by shifts (a
+    // runtime division per item made the sum ~3x slower than its shared-memory traffic).
+    // A thread takes the two fp32 column chunks 2cp, 2cp+1 of one row: their bf16 result is
+    // one 16-byte SW128 chunk, so 8 consecutive rows fill all 32 banks (one wavefront).
+    const int rs = 31 - __clz(R);
+    const int n_pairs = n_items / 2;
     // helper regions (tile, t) of this slice's rows: coalesced global loads (item -> 16 B,
     // consecutive threads -> consecutive rows of one column chunk)
     const float* const hreg = args.hzone + (size_t)tile * steps * (kChunks * 128 * 4) + sp * R * 4;
 #pragma unroll 1
-    for (int it0 = tid; it0 < n_items; it0 += 1024) {
-      float4 hv[2][4];
-      if (hx > 0) {
+    for (int p0 = tid; p0 < n_pairs; p0 += 512) {
 #pragma unroll
-        for (int t2 = 0; t2 < 2; ++t2)
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int it = it0 + 256 * q4;
-            hv[t2][q4] = t2 < steps ? ld_global_f4(hreg + (size_t)t2 * (kChunks * 128 * 4) + (size_t)(it / R) * 512 +
-                                                   (it % R) * 4)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-      }
-      float4 acc[4];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) acc[q4] = *reinterpret_cast<const float4*>(src + (it0 + 256 * q4) * 16);
+      for (int q2 = 0; q2 < 2; ++q2) {
+        const int pi = p0 + 256 * q2;
+        if (pi >= n_pairs) break;  // warp-uniform (n_pairs is a multiple of 256)
+        const int cp = pi >> rs, rr = pi & (R - 1);
+        const int it0 = (2 * cp) * R + rr, it1 = it0 + R;  // items (chunk 2cp, row rr), (2cp+1, rr)
+        float4 a0 = *reinterpret_cast<const float4*>(src + it0 * 16);
+        float4 a1 = *reinterpret_cast<const float4*>(src + it1 * 16);
 #pragma unroll 1
-      for (int j = 1; j < S; ++j) {  // splits in order
-        float4 f[4];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          f[q4] = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + (it0 + 256 * q4) * 16);
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          acc[q4].x += f[q4].x;
-          acc[q4].y += f[q4].y;
-          acc[q4].z += f[q4].z;
-          acc[q4].w += f[q4].w;
+        for (int j = 1; j < S; ++j) {  // splits in order
+          const float4 f0 = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + it0 * 16);
+          const float4 f1 = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + it1 * 16);
+          a0.x += f0.x; a0.y += f0.y; a0.z += f0.z; a0.w += f0.w;
+          a1.x += f1.x; a1.y += f1.y; a1.z += f1.z; a1.w += f1.w;
         }
-      }
-      if (hx > 0) {  // then the helpers' n-step partials, in order
-#pragma unroll
-        for (int t2 = 0; t2 < 2; ++t2)
-          if (t2 < steps)
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              acc[q4].x += hv[t2][q4].x;
-              acc[q4].y += hv[t2][q4].y;
-              acc[q4].z += hv[t2][q4].z;
-              acc[q4].w += hv[t2][q4].w;
-            }
-      }
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const int it = it0 + 256 * q4;
-        const int c = it / R, rr = it % R;
-        const int ch = (c % 16) / 2;
-        *reinterpret_cast<uint2*>(smem_gen + (ebuf - base) + (c / 16) * (R * 128) + rr * 128 + ((ch ^ (rr & 7)) << 4) +
-                                  (c & 1) * 8) =
-            make_uint2(pack2(args.f16, acc[q4].x, acc[q4].y), pack2(args.f16, acc[q4].z, acc[q4].w));
+        if (hx > 0) {  // then the helpers' n-step partials, in order
+          for (int t2 = 0; t2 < steps && t2 < 2; ++t2) {
+            const float* h = hreg + (size_t)t2 * (kChunks * 128 * 4) + rr * 4;
+            const float4 g0 = ld_global_f4(h + (size_t)(2 * cp) * 512), g1 = ld_global_f4(h + (size_t)(2 * cp + 1) * 512);
+            a0.x += g0.x; a0.y += g0.y; a0.z += g0.z; a0.w += g0.w;
+            a1.x += g1.x; a1.y += g1.y; a1.z += g1.z; a1.w += g1.w;
+          }
+        }
+        st_shared_v4(ebuf + (cp / 8) * (R * 128) + rr * 128 + (((cp % 8) ^ (rr & 7)) << 4),
+                     pack2(args.f16, a0.x, a0.y), pack2(args.f16, a0.z, a0.w), pack2(args.f16, a1.x, a1.y),
+                     pack2(args.f16, a1.z, a1.w));
       }
     }
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 22] = globaltimer_ns();
