@@ -101,7 +101,8 @@ def test_lowering_of_reference_top_plans(lib):
 
 @pytest.mark.parametrize("dims,kind", [((512, 8192, 2048, 2048), "gated_ffn"), ((512, 16384, 4096, 4096), "standard_ffn"),
                                        ((512, 3072, 768, 768), "standard_ffn"), ((3136, 64, 576, 256), "standard_ffn"),
-                                       ((4096, 8192, 2048, 2048), "standard_ffn"), ((200, 768, 256, 768), "standard_ffn")])
+                                       ((4096, 8192, 2048, 2048), "standard_ffn"), ((200, 768, 256, 768), "standard_ffn"),
+                                       ((512, 11008, 4096, 4096), "gated_ffn"), ((256, 8960, 1536, 1536), "standard_ffn")])
 def test_auto_config_invariants(lib, dims, kind):
     d = W.DimensionSpec(*dims, 2)
     graph = W.build_gated_ffn(d) if kind == "gated_ffn" else W.build_standard_ffn(d, "relu")
@@ -114,6 +115,22 @@ def test_auto_config_invariants(lib, dims, kind):
         _check_cfg(graph, cfg)
         ok += 1
     assert ok >= 1
+
+
+@pytest.mark.parametrize("dims,kind,expect", [
+    ((512, 11008, 4096, 4096), "gated_ffn", (16, 2, 3)),      # LLaMA-7B: 86 chunks, 43 per split, last step 11 of 16
+    ((256, 8960, 1536, 1536), "standard_ffn", (6, 4, 2)),     # 35 chunks: splits of 9, 9, 9, 8
+    ((512, 16384, 4096, 4096), "standard_ffn", (16, 2, 2)),   # whole steps: unchanged
+])
+def test_pair_lowering_takes_ragged_rings(lib, dims, kind, expect):
+    """The pair transport keeps the widest ring when N / nb is not a ring multiple
+    (ceil(chunks / S) chunks per split, ragged last n-step) instead of falling back
+    to l clusters that recompute GEMM0."""
+    d = W.DimensionSpec(*dims, 2)
+    graph = W.build_gated_ffn(d) if kind == "gated_ffn" else W.build_standard_ffn(d, "relu")
+    cfg = runtime.lower(graph, None, 148, "pair")
+    assert (cfg.ring, cfg.n_splits, cfg.steps) == expect and cfg.l_clusters == 1
+    _check_cfg(graph, cfg)
 
 
 def test_status_codes_map_to_reference_exceptions(lib):
