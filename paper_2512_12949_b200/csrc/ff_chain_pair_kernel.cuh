@@ -654,7 +654,8 @@ __global__ void __launch_bounds__(256, 1)
     const unsigned long long t_start = clock64();
     // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
     auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
-    for (int T = 0; T < total_steps; ++T) {
+    // C chunk of global step T: TMEM -> activation / gate -> bf16 SW128 own slot -> L2 scratch + flag
+    auto drain_c = [&](int T) {
       const Unit u = unit_of(T / steps);
       const int t = T % steps;
       FF_TIMED(w_cfull, (swap_e && T == 1) ? mbar_wait_cluster(c_full1, 0) : mbar_wait_cluster(c_full, T & 1));
@@ -732,14 +733,31 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (args.prof) t_store += clock64() - t_s0;
       if (issuer && T < 2) FF_STAMP(20 + 3 * T);
+    };
+    int next_c = 0;  // first C chunk not yet drained
+    for (int T = 0; T < total_steps; ++T) {
+      if (next_c <= T) {
+        drain_c(T);
+        next_c = T + 1;
+      }
+      const Unit u = unit_of(T / steps);
+      const int t = T % steps;
       if (t == steps - 1 && !(scatter_all && T == total_steps - 1)) {
+        // The next unit's first C chunk is ready mid-way through this unit's last hops:
+        // drain and publish it before this unit's E, so the tensor core can start the
+        // next GEMM0 while E drains (not with kOwnFull: the own slot then still holds
+        // that chunk as hop 0's operand when E needs it for staging).
+        if (!C::kOwnFull && T + 1 < total_steps && !(args.dbg & (1u << 31))) {
+          drain_c(T + 1);
+          next_c = T + 2;
+        }
         // E slice: TMEM -> registers -> SW128 smem tiles in the own slot -> TMA
         // store (bf16) or TMA reduce-add into the fp32 workspace (N splits).
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
         mbar_wait_cluster(e_full, (T / steps) & 1);
         tc_fence_after();
         if (issuer) FF_STAMP(30);
-        mbar_wait_cluster(own_free, T & 1);  // own slot no longer read by hop 0 / the C store
+        mbar_wait_cluster(own_free, (next_c - 1) & 1);  // own slot no longer read by hop 0 / the last C store
         const int erow = u.m0 + (int)q * C::BM;
         // Staging: the own slot (2 x 16 KB tiles), or -- for the ring's final
         // unit, when every pipeline stage has been consumed (e_full) and no
@@ -817,6 +835,10 @@ __global__ void __launch_bounds__(256, 1)
                              __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
             }
           }
+          if (g1 == kLB) {  // every E column read: the next unit's hops may start (before the last store)
+            tc_fence_before();
+            mbar_arrive_remote(L_e_empty);
+          }
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
           if (issuer) {
@@ -832,8 +854,6 @@ __global__ void __launch_bounds__(256, 1)
           }
           named_bar_sync(1, 128);
         }
-        tc_fence_before();
-        mbar_arrive_remote(L_e_empty);
         if (issuer) FF_STAMP(24);
         if (!bf16_out) {
           split_finish<kLB>(args, tile_counter, tmem_slot + 8, issuer, true, erow, row, u.l0, 1, false);
