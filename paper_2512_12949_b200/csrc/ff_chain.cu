@@ -282,9 +282,22 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   const CUtensorMapDataType dt = elem_type(ch);
   bool ok = implicit ? make_map_im2col(&mA, t->a, conv->ic, conv->w, conv->h, conv->batch, conv->k1, dt)
                      : make_map(&mA, t->a, M, K, 64, 128, dt);
-  ok = ok && make_map(&mB0, t->b, K, N, 64, 64, dt);
+  // B (standard chains) and D as 3D views {64 columns, rows, column blocks}: one TMA box fetches
+  // every 64-column block of a stage (kNB/64 or kLB/64 tiles of [64 rows][64 cols], 8 KB apart)
+  if (kGated) {
+    ok = ok && make_map(&mB0, t->b, K, N, 64, 64, dt);
+  } else {
+    const uint64_t db[3] = {64, K, N / 64}, sb[2] = {N * 2, 128};
+    const uint32_t bb[3] = {64, 64, kNB / 64};
+    ok = ok && make_map_nd(&mB0, dt, 3, t->b, db, sb, bb);
+  }
   ok = ok && make_map(&mB1, kGated ? t->b1 : t->b, K, N, 64, 64, dt);
-  ok = ok && make_map(&mD, t->d, conv2 ? (uint64_t)conv->k2 * conv->k2 * N : N, L, 64, 64, dt);
+  {
+    const uint64_t drows = conv2 ? (uint64_t)conv->k2 * conv->k2 * N : N;
+    const uint64_t dd[3] = {64, drows, L / 64}, sd[2] = {L * 2, 128};
+    const uint32_t bd[3] = {64, 64, kLB / 64};
+    ok = ok && make_map_nd(&mD, dt, 3, t->d, dd, sd, bd);
+  }
   const bool l2x = (kMode == ff::XCHG_L2 && cfg->ring > 1);
   const bool cs = l2x || conv2;  // C scratch in use: [m_tiles*128][N] 2D view (publish stores, ring hops)
   ok = ok && make_map(&mCs, cs ? (const void*)(wsb + wl.c_off) : t->a, cs ? (uint64_t)cfg->m_tiles * 128 : M,

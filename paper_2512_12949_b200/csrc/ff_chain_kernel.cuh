@@ -409,9 +409,8 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_2d(sb + C::kA_BYTES, &tmB0, full_bar(stage), n0, kb * C::BK);
             tma_load_2d(sb + C::kA_BYTES + C::BK * kNB * 2, &tmB1, full_bar(stage), n0, kb * C::BK);
           } else {
-#pragma unroll
-            for (int j = 0; j < kNB / 64; ++j)
-              tma_load_2d(sb + C::kA_BYTES + j * 8192, &tmB0, full_bar(stage), n0 + 64 * j, kb * C::BK);
+            // one 3D box: kNB/64 MN-major [64 k x 64 n] tiles 8 KB apart (TMA is per-instruction bound)
+            tma_load_3d(sb + C::kA_BYTES, &tmB0, full_bar(stage), 0, kb * C::BK, n0 / 64);
           }
           next();
         }
@@ -440,9 +439,7 @@ __global__ void __launch_bounds__(256, 1)
             mbar_expect_tx(full_bar(stage), C::kG1_BYTES);
             tma_load_im2col_4d(sb, &tmC, full_bar(stage), cb * 64, rem % W - pad, rem / W - pad, img,
                                (uint16_t)(tap % args.conv2_k), (uint16_t)(tap / args.conv2_k));
-#pragma unroll
-            for (int j = 0; j < kLB / 64; ++j)
-              tma_load_2d(sb + C::kG1_DOFF + j * 8192, &tmD, full_bar(stage), u.l0 + 64 * j, kb2 * C::BK);
+            tma_load_3d(sb + C::kG1_DOFF, &tmD, full_bar(stage), 0, kb2 * C::BK, u.l0 / 64);
             next();
           }
           return;
@@ -464,9 +461,7 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), remote_c ? C::kG1_BYTES : C::kD_BYTES);
           if (remote_c) tma_load_2d(sb, &tmC, full_bar(stage), nrow0 + kb2 * C::BK, u.m0);
-#pragma unroll
-          for (int j = 0; j < kLB / 64; ++j)
-            tma_load_2d(sb + C::kG1_DOFF + j * 8192, &tmD, full_bar(stage), u.l0 + 64 * j, nrow0 + kb2 * C::BK);
+          tma_load_3d(sb + C::kG1_DOFF, &tmD, full_bar(stage), 0, nrow0 + kb2 * C::BK, u.l0 / 64);
           next();
         }
       };
