@@ -516,7 +516,9 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
                            d, st, b);
   }
   {  // whole-tile / row-slice 3D views of E and the fp32 workspace (final-unit epilogue)
-    const uint32_t rs = 128u / (uint32_t)std::max(1, cfg->n_splits);  // split row slice
+    // split row slice (the reduce-scatter tail needs S <= 8, pair_finish_regions; the maps
+    // are encoded for every launch, so keep their boxes legal for any S)
+    const uint32_t rs = std::max(1u, 128u / (uint32_t)std::max(1, cfg->n_splits));
     const uint64_t de[3] = {64, M, L / 64}, se[2] = {L * 2, 128};
     const uint32_t be[3] = {64, 128, 256 / 64}, ber[3] = {64, rs, 256 / 64};
     ok = ok && make_map_nd(&maps.e3, BF, 3, t->e, de, se, be);
@@ -532,7 +534,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const void* sp = cfg->n_splits > 1 ? (const void*)(wsb + wl.s_off) : t->e;
     const uint64_t tiles = (uint64_t)cfg->m_tiles * 2 * (L / 256);
     const uint64_t ds[3] = {32, 16, tiles * S * 64}, ss[2] = {128, 2048};
-    const uint32_t bs[3] = {32, rs / 8, 64};
+    const uint32_t bs[3] = {32, std::max(1u, rs / 8), 64};
     ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sp, ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
   }
     if (ok) {

@@ -331,6 +331,22 @@ def test_auto_lowering_with_ragged_ring(case):
     _check(kind, act, host, out)
 
 
+def test_pair_many_splits_small_m():
+    """Tiny M with a wide N lowers to 32 N splits of a ring of one pair; the tail's
+    exchange-region maps (unused beyond 8 splits) once got an illegal zero-row box
+    (found by tests/_fuzz_gpu.py)."""
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = "gated_ffn", "silu", 40, 4096, 768, 256
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = runtime.lower(graph, None, 148, "pair")
+    assert cfg.n_splits > 8
+    host, dev = _inputs(kind, m, n, k, l, seed=31)
+    out = runtime.launch(graph, cfg, dev)
+    _torch().cuda.synchronize()
+    _check(kind, act, host, out)
+
+
 def test_workspace_zero_invariant_across_configs():
     """The split counters and the fp32 E zone of the shared per-stream workspace
     are zero after every launch (configs reuse one workspace; a config whose
