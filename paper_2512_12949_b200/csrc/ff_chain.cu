@@ -636,9 +636,13 @@ bool quad_ok(const ffKernelConfig* cfg) {
   if (g_dbg & 64u) return false;  // diagnostics: force the plain pair kernel
   if (cfg->helpers > 0) return false;  // helper pairs fill the SMs a cluster-of-4 launch cannot
   if (cfg->m_tiles % 2 || cfg->units % 2) return false;
-  int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
-  rings = std::min(rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring));
-  return rings >= 2;
+  const int pair_rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
+  int rings = std::min(pair_rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring)) & ~1;
+  if (rings < 2) return false;
+  // quads need an even ring count: when that costs a wave of units (OPT M=32768: 128 units
+  // on 8 quad rings = 16 waves vs 9 pair rings = 15), plain pairs win (-2.4 %, A/B)
+  const int waves_quad = (cfg->units + rings - 1) / rings, waves_pair = (cfg->units + pair_rings - 1) / pair_rings;
+  return waves_quad <= waves_pair;
 }
 
 template <bool kGated, bool kPacked>
