@@ -436,8 +436,15 @@ def test_one_cta_region_finish_matches_oracle_and_repeats_bitwise(case, exchange
     assert torch.equal(out1, out2)
 
 
-@pytest.mark.parametrize("exchange", ["pair", "l2", "dsm"])
-def test_cuda_graph_capture_replays_the_chain(exchange):
+@pytest.mark.parametrize("exchange,case", [("pair", ("gated_ffn", "silu", 512, 8192, 2048, 2048)),
+                                           ("l2", ("gated_ffn", "silu", 512, 8192, 2048, 2048)),
+                                           ("dsm", ("gated_ffn", "silu", 512, 8192, 2048, 2048)),
+                                           # multi-unit rings (16 units on 9 rings): unit-boundary reorder
+                                           ("pair", ("standard_ffn", "relu", 4096, 2048, 512, 2048)),
+                                           # ragged ring (N = 11 chunks on a ring of 4 pairs)
+                                           ("pair", ("standard_ffn", "gelu", 384, 2816, 256, 1024))],
+                         ids=["pair", "l2", "dsm", "pair-multi-unit", "pair-ragged"])
+def test_cuda_graph_capture_replays_the_chain(exchange, case):
     """Stream capture of runtime.launch (no host sync, caller-owned workspace per
     stream).  Every replay must see a fresh launch epoch (kept on the device): the
     inputs change between replays, so a stale ready flag would leak the previous
@@ -445,7 +452,7 @@ def test_cuda_graph_capture_replays_the_chain(exchange):
     torch = _torch()
     from paper_2512_12949_b200 import runtime
 
-    kind, act, m, n, k, l = ("gated_ffn", "silu", 512, 8192, 2048, 2048)
+    kind, act, m, n, k, l = case
     graph = _graph(kind, act, m, n, k, l)
     cfg = runtime.lower(graph, None, 148, exchange)
     host, dev = _inputs(kind, m, n, k, l, seed=21)
