@@ -582,7 +582,10 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   // hops deferred past GEMM0(T+1): about one C drain (+ its store for the
   // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
-  a.defer = cfg->ring - 1 - cfg->ring / 4;  // measured: 3/4 of the hops (profiles/r01/cfgs_defer.log)
+  // GEMM0 of step t+1 entirely before the remote hops of step t (defer = G-1): since the epilogue
+  // drains C ahead of E at unit boundaries this beats spreading it over the first G/4 hops
+  // (OPT M=4096 -1.5 %, A/B; profiles/r01/cfgs_defer.log had 3/4 before that change)
+  a.defer = cfg->ring - 1;
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
   a.finish_tma = pair_finish_regions(ch, cfg, rings);
   // helper pairs (planned by finish_config for the non-quad launch)
