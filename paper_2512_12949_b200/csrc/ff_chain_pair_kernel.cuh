@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(256, 1)
 
   // GEMM0 of step T+1 is spread over the first G - defer hops of step T; the
   // last `defer` hops run after it, while the epilogue drains C(T+1), so the
-  // tensor core does not idle through the drain.
-  // The ring's last GEMM0 runs before every hop of the previous step: nothing
-  // follows it, so all G-1 remote hops are needed to cover its drain, publish
-  // and the ring members' skew.
+  // tensor core does not idle through the drain.  The host sets defer = G-1
+  // (one slice: GEMM0(T+1) before every hop of step T); the ring's last GEMM0
+  // always runs that way (defer_last): nothing follows it, so all hops are
+  // needed to cover its drain, publish and the ring members' skew.
   auto slot_lo = [&](int Tn, int h) {
     const int g0_slices = (Tn == total_steps - 1 && args.defer_last) ? 1 : G - args.defer;
     return h < g0_slices ? h * kblocks / g0_slices : kblocks;
