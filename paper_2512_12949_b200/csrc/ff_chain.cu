@@ -635,16 +635,20 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
 // Quad (weight-multicast) variant when the units come in m-tile couples that
 // share their weights: an even number of m tiles, an even number of rings of
 // at most one unit each... any even ring count works (units 2j / 2j+1 pair up).
-bool quad_ok(const ffKernelConfig* cfg) {
+bool quad_ok(const ffKernelConfig* cfg, bool gated) {
   if (g_dbg & 64u) return false;  // diagnostics: force the plain pair kernel
   if (cfg->helpers > 0) return false;  // helper pairs fill the SMs a cluster-of-4 launch cannot
   if (cfg->m_tiles % 2 || cfg->units % 2) return false;
   const int pair_rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
   int rings = std::min(pair_rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring)) & ~1;
   if (rings < 2) return false;
+  if (g_dbg & (1u << 21)) return true;  // diagnostics / tests: quad whenever it can launch
   // quads need an even ring count: when that costs a wave of units (OPT M=32768: 128 units
   // on 8 quad rings = 16 waves vs 9 pair rings = 15), plain pairs win (-2.4 %, A/B)
   const int waves_quad = (cfg->units + rings - 1) / rings, waves_pair = (cfg->units + pair_rings - 1) / pair_rings;
+  // (gated one-wave chains: plain pairs 0.35 us faster than quads on one box, 0.08 us slower
+  // on another -- no rule; quads stay the default)
+  (void)gated;
   return waves_quad <= waves_pair;
 }
 
@@ -654,7 +658,7 @@ int launch_pair_q(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTens
   // ragged n-steps (N not a whole number of ring steps per split): plain pairs only
   if (ch->n != (int64_t)cfg->n_splits * cfg->steps * cfg->ring * cfg->nb)
     return launch_pair_impl<kGated, kPacked, false, true>(ch, cfg, t, ws, c_debug, stream, conv);
-  return quad_ok(cfg) ? launch_pair_impl<kGated, kPacked, true, false>(ch, cfg, t, ws, c_debug, stream, conv)
+  return quad_ok(cfg, kGated) ? launch_pair_impl<kGated, kPacked, true, false>(ch, cfg, t, ws, c_debug, stream, conv)
                       : launch_pair_impl<kGated, kPacked, false, false>(ch, cfg, t, ws, c_debug, stream, conv);
 }
 

@@ -230,7 +230,7 @@ def test_split_reduction_leaves_workspace_zero(exchange, ring, splits, nb, lb):
 
 # pair-kernel variants behind debug bits (ff_set_debug_mode): helper pairs on the idle
 # SMs (bit 26, opt-in), common GEMM0 k order (bit 27), plain pair kernel (bit 6)
-@pytest.mark.parametrize("mode", [1 << 26, 1 << 27, 64], ids=["helpers", "no-krot", "no-quad"])
+@pytest.mark.parametrize("mode", [1 << 26, 1 << 27, 64, 1 << 21], ids=["helpers", "no-krot", "no-quad", "force-quad"])
 @pytest.mark.parametrize("case", [("gated_ffn", "silu", 512, 8192, 2048, 2048),
                                   ("standard_ffn", "relu", 512, 16384, 4096, 4096)], ids=["llama1b", "gpt67b"])
 def test_pair_kernel_variants_match_oracle_and_repeat_bitwise(case, mode):
