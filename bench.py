@@ -1,21 +1,24 @@
 """Benchmark of the fused GEMM-chain hot path on B200.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload llama1b]
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload gpt67b]
 
 One "step" = one fused chain (GEMM0 -> act/SwiGLU gate -> GEMM1) over one
-batch of M=512 tokens with the weights resident in HBM.  At N>1 (torchrun,
-one rank per GPU) every rank runs its own batch: the token dimension shards
-with no collective on the data path ("scaling": "weak").
+batch of tokens with the weights resident in HBM.  At N>1 (torchrun, one rank
+per GPU) every rank runs its own batch: the token dimension shards with no
+collective on the data path ("scaling": "weak"; opt13b_m32768 is the
+strong-scaling sweep of BASELINE.json configs[4]).
 
-Workload (BASELINE.json configs[1]): LLaMA-1B gated SwiGLU FFN, M=512,
-2048 -> 8192 -> 2048, bf16 storage / fp32 accumulation.  The L2 (126 MB) is
-flushed between timed steps (the weights alone are 96 MiB).
+Headline workload: the north-star chain, GPT-6.7B FFN M=512, 4096 -> 16384 ->
+4096 (BASELINE.json configs[2]), bf16 storage / fp32 accumulation, in ONE
+sm_100a kernel.  The L2 (126 MB) is flushed between timed steps.
 
-JSON keys beyond the base contract: roofline (dominant kernel vs the measured
-bf16 peak), cpu_baseline (the reference CPU path, oracle port, timed on this
-host), e2e (public API with pinned host buffers), cublas_unfused (same config
-through torch.matmul), hbm (algorithmic bytes fused vs unfused), extra (the
-other BASELINE configs, single GPU, same method).
+JSON keys beyond the base contract: fused_vs_cublas (the fused kernel against the
+fastest unfused cuBLAS variant), cublas_unfused (eager and CUDA-graph, separate and
+fused-epilogue activation / packed gate|up), roofline (dominant kernel vs the
+measured bf16 peak), hbm (analyzer-predicted, unfused-model, algorithmic and
+ncu-measured DRAM bytes), cpu_baseline (the reference's CPU path from
+baseline/_ref, timed on this host), e2e (public API with pinned host buffers),
+extra (the other BASELINE configs, single GPU, same method).
 """
 
 from __future__ import annotations
@@ -59,7 +62,7 @@ def rank_rows(name, world, rank=0):
 
     lo, hi = sharding.shard_bounds(m, world, rank)
     return hi - lo
-DEFAULT_WORKLOAD = "llama1b"
+DEFAULT_WORKLOAD = "gpt67b"
 
 
 def flops_of(kind, m, n, k, l):
@@ -194,35 +197,85 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU baseline
 
 
-def cpu_reference_step(kind, act, m, n, k, l, inputs, plan_doc):
-    """One execution of the reference's CPU path for the chain: the plan-faithful
-    tile replay (fuseplan simulate) restated in oracle/ (numpy BLAS, f32)."""
-    import oracle
-
-    return oracle.replay_plan(kind, act, (m, n, k, l), plan_doc, inputs)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")  # the UNMODIFIED reference (pip --target install)
 
 
-def cpu_baseline(name, steps=None, budget_s=12.0):
-    """Time the oracle port of the reference CPU path on a bounded sample."""
-    import oracle
+def _reference_modules():
+    """fuseplan from baseline/_ref (the reference's own code, installed unmodified);
+    None when that install is absent (then the oracle port stands in)."""
+    if not os.path.isdir(os.path.join(REF_PATH, "fuseplan")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import fuseplan.hardware as rh
+    import fuseplan.plan as rp
+    import fuseplan.simulator as rs
+    import fuseplan.workload as rw
 
+    return rw, rp, rs, rh
+
+
+def _reference_device(rh):
+    """The B200 profile as a reference DeviceModel.  The reference parser rejects the
+    measured DSM table (DSM below HBM per SM on B200), so the model is
+    built from the same numbers directly, as tests/golden/make_golden.py does."""
+    from paper_2512_12949_b200.hardware import b200_profile
+
+    p = b200_profile()
+    lvl = lambda m: rh.MemoryLevel(m.name, m.scope, m.capacity_bytes, m.bandwidth)  # noqa: E731
+    return rh.DeviceModel(name=p.name, reg=lvl(p.reg), smem=lvl(p.smem), dsm_bandwidth_table=dict(p.dsm_bandwidth_table),
+                          l2=lvl(p.l2), global_mem=lvl(p.global_mem), max_cluster_blocks=p.max_cluster_blocks,
+                          cluster_dim_options=tuple(p.cluster_dim_options), mma_tile=tuple(p.mma_tile))
+
+
+def reference_cpu_step(name, rows, seed=0):
+    """One plan-faithful execution of the chain on the host by the reference's CPU
+    path: fuseplan.simulator.execute_plan (simulator.py:177-424, numpy f32 BLAS) from
+    baseline/_ref under the reference search's top-1 plan, on a `rows`-token sample.
+    Returns (callable, kind, path description)."""
     kind, act, m, n, k, l, _ = WORKLOADS[name]
-    plan_doc = _reference_plan(name)
-    rows = m if m <= 512 else 512          # bounded sample: at most 512 token rows
-    inputs = oracle.make_inputs(kind, rows, n, k, l, seed=0, dtype=np.float32)
-    cpu_reference_step(kind, act, rows, n, k, l, inputs, _rows_plan(plan_doc, rows))  # warm-up
+    plan_doc = _rows_plan(_reference_plan(name), rows)
+    mods = _reference_modules()
+    if mods is not None:
+        rw, rp, rs, rh = mods
+        dims = rw.DimensionSpec(rows, n, k, l, 2)
+        # GELU has no reference counterpart: its chain runs with ReLU (same loop nest and bytes)
+        graph = rw.build_gated_ffn(dims) if kind == "gated_ffn" else rw.build_standard_ffn(
+            dims, "relu" if act == "gelu" else act)
+        plan = rp.plan_from_dict(plan_doc)
+        config = rs.SimConfig(dtype="f32", seed=seed, max_workspace_bytes=8 << 30)
+        inputs = rs.make_inputs(graph, config)
+        device = _reference_device(rh)
+
+        def step():
+            rs.execute_plan(plan, graph, inputs, config, device)
+        return step, "reference", "fuseplan.simulator.execute_plan from baseline/_ref (unmodified reference, f32)"
+    import oracle
+
+    inputs = oracle.make_inputs(kind, rows, n, k, l, seed=seed, dtype=np.float32)
+
+    def step():
+        oracle.replay_plan(kind, act, (rows, n, k, l), plan_doc, inputs)
+    return step, "port", "oracle.replay_plan (numpy restatement of simulator.execute_plan, f32)"
+
+
+def cpu_baseline(name, budget_s=12.0):
+    """Time the reference CPU path on a bounded sample (at most 512 token rows)."""
+    kind, act, m, n, k, l, _ = WORKLOADS[name]
+    rows = m if m <= 512 else 512
+    step, cpu_kind, path = reference_cpu_step(name, rows)
+    step()  # warm-up
     times = []
     t_end = time.perf_counter() + budget_s
-    while (steps is None and time.perf_counter() < t_end and len(times) < 20) or (steps is not None and len(times) < steps):
+    while time.perf_counter() < t_end and len(times) < 20:
         t0 = time.perf_counter()
-        cpu_reference_step(kind, act, rows, n, k, l, inputs, _rows_plan(plan_doc, rows))
+        step()
         times.append(time.perf_counter() - t0)
     sec = float(np.median(times))
-    threads = _blas_threads()
-    return {"value": flops_of(kind, rows, n, k, l) / sec / 1e12, "unit": "TFLOP/s", "cores": threads,
-            "kind": "port", "seconds_per_chain": sec, "runs": len(times),
-            "sample": f"{len(times)} plan-faithful replays (oracle.replay_plan, numpy f32 BLAS) of "
-                      f"{kind} m={rows} n={n} k={k} l={l} under the reference top-1 plan (B200 profile)"}
+    return {"value": flops_of(kind, rows, n, k, l) / sec / 1e12, "unit": "TFLOP/s", "cores": _blas_threads(),
+            "kind": cpu_kind, "seconds_per_chain": sec, "runs": len(times),
+            "sample": f"{len(times)} runs of {path} on {kind} m={rows} n={n} k={k} l={l} under the reference "
+                      f"search's top-1 plan (B200 profile)"}
 
 
 def _blas_threads():
@@ -270,6 +323,7 @@ def make_device_inputs(kind, m, n, k, l, seed, device):
     import torch
 
     g = torch.Generator(device="cpu").manual_seed(seed)
+
     def u(*shape):
         return (torch.rand(*shape, generator=g) * 2 - 1).to(torch.bfloat16).to(device)
     t = {"A": u(m, k), "D": u(n, l)}
@@ -292,42 +346,61 @@ def graph_of(name, m=None):
     return W.build_gated_ffn(dims) if kind == "gated_ffn" else W.build_standard_ffn(dims, act)
 
 
-def choose_config(name, tensors, profile=True, m=None):
-    """Plan -> physical launch: top-K reference plans (plan cache) lowered and timed
-    on the device (ProfileBestFromList), plus the runtime's hardware-shaped config.
-    profile=False (ncu launch lists): the shipped M-bin dispatch table's entry."""
+def _plans_of(name, m):
+    from paper_2512_12949_b200 import plan_cache
+    from paper_2512_12949_b200.plan import plan_from_dict
+
+    kind, act, _, n, k, l, _ = WORKLOADS[name]
+    entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
+    return [plan_from_dict(p) for p in entry["top"]] if entry else []
+
+
+def choose_config(name, tensors, profile=True, m=None, flush=None):
+    """Plan -> physical launch, ProfileBestFromList (Alg. 2 line 10): the reference
+    search's top-K plans (plan cache) lowered under every transport, plus the runtime's
+    hardware-shaped lowering, deduplicated and timed on the device (L2 flushed before
+    every launch, median of 7); the fastest runs.  Returns (cfg, label, plan or None,
+    candidates).  profile=False (ncu launch lists): the shipped M-bin dispatch table."""
+    from paper_2512_12949_b200 import runtime
+
     m = WORKLOADS[name][2] if m is None else m
+    graph = graph_of(name, m)
     if not profile:
         from paper_2512_12949_b200 import dispatch
 
         fam = {"llama1b": "llama1b", "gpt67b": "gpt67b", "gpt2s": "gpt2s", "opt13b_m4096": "opt13b",
                "opt13b_m32768": "opt13b"}[name]
         table = dispatch.shipped(fam)
+        plans = _plans_of(name, m)
         if m <= table.bins[-1]:
-            return table.config_for(m), f"dispatch table [{fam}, M bin of {m}]", []
-        from paper_2512_12949_b200 import runtime
+            return table.config_for(m), f"dispatch table [{fam}, M bin of {m}]", (plans[0] if plans else None), []
+        return runtime.lower(graph, None), "runtime-auto (beyond the dispatch table)", None, []
+    import torch
 
-        return runtime.lower(graph_of(name, m), None), "runtime-auto (beyond the dispatch table)", []
-    from paper_2512_12949_b200 import plan_cache, runtime
-    from paper_2512_12949_b200.plan import plan_from_dict
-
-    graph = graph_of(name, m)
-    kind, act, _, n, k, l, _ = WORKLOADS[name]
-    cands = []
-    entry = plan_cache.lookup(kind, "relu" if act == "gelu" else act, m, n, k, l)
-    plans = [plan_from_dict(p) for p in entry["top"]] if entry else []
-    timed = runtime.profile_best_from_list(graph, plans, tensors, iters=5, warmup=2,
-                                           exchanges=("pair", "l2", "dsm")) if plans else []
-    cands += [(ms, cfg, f"{plan.describe()} [{runtime.exchange_name(cfg)}]") for ms, plan, cfg in timed]
-    for exchange in ("pair", "l2", "dsm"):
+    plans = _plans_of(name, m)
+    cands = {}  # config key -> [cfg, labels, plan]
+    for plan, x in [(p, x) for p in plans for x in ("pair", "l2", "dsm")] + [(None, x) for x in ("pair", "l2", "dsm")]:
         try:
-            auto = runtime.lower(graph, None, exchange=exchange)
+            cfg = runtime.lower(graph, plan, 148, x)
         except Exception:
             continue
-        ms_auto = runtime.profile_configs(graph, [auto], tensors, iters=5, warmup=2)[0][0]
-        cands.append((ms_auto, auto, f"runtime-auto [{exchange}]"))
-    cands.sort(key=lambda c: c[0])
-    return cands[0][1], cands[0][2], [(round(c[0] * 1e3, 2), c[2]) for c in cands]
+        key = tuple(sorted(cfg.as_dict().items()))
+        label = f"{plan.describe()} [{x}]" if plan is not None else f"runtime-auto [{x}]"
+        if key in cands:
+            cands[key][1].append(label)
+        else:
+            cands[key] = [cfg, [label], plan]
+    out = torch.empty((m, WORKLOADS[name][5]), dtype=torch.bfloat16, device=tensors["A"].device)
+    flush = flush or (lambda: None)
+    timed = []
+    for cfg, labels, plan in cands.values():
+        fn = lambda: runtime.launch(graph, cfg, tensors, out=out)  # noqa: E731
+        fn()
+        ms = float(np.median(time_steps(fn, 7, flush, torch.cuda.current_stream())))
+        timed.append((ms, cfg, labels, plan))
+    timed.sort(key=lambda c: c[0])
+    ms, cfg, labels, plan = timed[0]
+    return cfg, " = ".join(labels), plan, [(round(c[0] * 1e3, 2), " = ".join(c[2])) for c in timed]
 
 
 def time_steps(fn, steps, flush, stream):
@@ -422,6 +495,38 @@ def _max_over_ranks(x, dev):
     return float(t.item())
 
 
+def hbm_table(name, plan, m=None):
+    """Four byte counts per chain: the analyzer's predicted
+    global-tier volume for the executed plan (analyzer.py:413-489), the reference's
+    unfused two-kernel byte model for the same plan (simulator.py:495-556), and the
+    ncu-measured DRAM bytes of the fused launch and of the cuBLAS path (write-backs of
+    dirty lines counted, tools/dram_bytes.py), beside the algorithmic minimum."""
+    from paper_2512_12949_b200.analyzer import analyze
+    from paper_2512_12949_b200.hardware import b200_profile
+    from paper_2512_12949_b200.simulator import unfused_traffic
+
+    kind, act, m0, n, k, l, _ = WORKLOADS[name]
+    m = m0 if m is None else m
+    fused_b, unfused_b = hbm_bytes(kind, m, n, k, l)
+    row = {"algorithmic_fused_bytes": fused_b, "algorithmic_unfused_bytes": unfused_b}
+    if plan is not None:
+        graph = graph_of(name, m)
+        try:
+            row["analyzer_global_bytes"] = int(analyze(graph, b200_profile(), plan).volume["global"])
+            row["unfused_model_bytes"] = int(unfused_traffic(graph, plan).tier_bytes["global"])
+            row["plan"] = plan.describe()
+        except Exception as exc:  # informative only
+            row["analyzer_error"] = repr(exc)
+    ncu = load_ncu_summary(name)
+    row["ncu_fused_dram_bytes"] = ncu.get("fused", {}).get("dram_total")
+    row["ncu_cublas_dram_bytes"] = ncu.get("cublas", {}).get("dram_total")
+    if row["ncu_fused_dram_bytes"] and row["ncu_cublas_dram_bytes"]:
+        row["ncu_fused_over_cublas"] = round(row["ncu_fused_dram_bytes"] / row["ncu_cublas_dram_bytes"], 4)
+        row["ncu_fused_over_algorithmic"] = round(row["ncu_fused_dram_bytes"] / fused_b, 4)
+    row["source"] = ncu.get("source")
+    return row
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -442,7 +547,7 @@ def run_ours(args, rank, world, local_rank):
         flush_buf.add_(1.0)
 
     stream = torch.cuda.current_stream(dev)
-    cfg, cfg_name, candidates = choose_config(name, tensors, profile=not args.no_profile_plans, m=m)
+    cfg, cfg_name, plan, candidates = choose_config(name, tensors, profile=not args.no_profile_plans, m=m, flush=flush)
     out = torch.empty((m, l), dtype=torch.bfloat16, device=dev)
 
     def step():
@@ -500,16 +605,15 @@ def run_ours(args, rank, world, local_rank):
         e2e_pipe["ms_total"] = _max_over_ranks(e2e_pipe["ms_total"], dev)
     e2e_pipe_value = job_fl * args.steps / (e2e_pipe["ms_total"] * 1e-3) / 1e12
 
-    # unfused cuBLAS on the same config
-    cub = cublas_unfused(kind, act, tensors, flush, stream, max(args.steps, 5))
+    # unfused cuBLAS on the same config (eager and CUDA-graph, separate and fused-epilogue activation)
+    cub = cublas_unfused(kind, act, tensors, flush, stream, max(min(args.steps, 50), 10))
 
     if rank != 0:
         return None
     peaks = load_peaks()
     kern_ms = float(np.median(times))
     achieved = fl / (kern_ms * 1e-3) / 1e12
-    fused_b, unfused_b = hbm_bytes(kind, m, n, k, l)
-    ncu = load_ncu_summary(name)
+    hbm = hbm_table(name, plan, m)
     launches = runtime.kernel_launches(graph, cfg) * args.steps
     doc = {
         "metric": METRIC,
@@ -529,9 +633,12 @@ def run_ours(args, rank, world, local_rank):
                    "parallelism": f"token-sharded x{world} (independent per GPU)",
                    "l2": "flushed between timed steps (256 MiB write)", "launch": cfg.as_dict(),
                    "plan": cfg_name, "candidates_ms": candidates},
+        "fused_vs_cublas": {"fused_ms": round(kern_ms, 4), "cublas_best_ms": cub["best_ms"],
+                            "cublas_best": cub["best"], "speedup": round(cub["best_ms"] / kern_ms, 4),
+                            "cublas_eager_ms": cub["variants"]["eager"]["ms"]},
         "roofline": {"bound": "tensor", "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"],
                      "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 4),
-                     "traffic": ncu.get("dram_bytes_per_launch"), "peak_source": peaks["source"],
+                     "traffic": hbm.get("ncu_fused_dram_bytes"), "peak_source": peaks["source"],
                      "kernel_ms_median": round(kern_ms, 4)},
         "e2e": {"value": round(e2e_pipe_value, 2), "unit": "TFLOP/s", "h2d_bytes_per_step": int(host_a.numel() * 2),
                 "d2h_bytes_per_step": int(host_e.numel() * 2),
@@ -544,57 +651,126 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk,
         "cublas_unfused": cub,
-        "hbm": {"algorithmic_fused_bytes": fused_b, "algorithmic_unfused_bytes": unfused_b,
-                "ncu_fused_dram_bytes": ncu.get("dram_bytes_per_launch"),
-                "ncu_unfused_dram_bytes": ncu.get("cublas_dram_bytes"), "source": ncu.get("source")},
+        "hbm": hbm,
         "wall_s_timed": round(wall, 3),
     }
     return doc
 
 
-def cublas_unfused(kind, act, t, flush, stream, steps):
+def _silu_and_mul():
+    """Production SwiGLU kernel for the packed baseline: vLLM's silu_and_mul (one
+    fused elementwise kernel over [M, 2N] -> [M, N]) when its extension loads; else
+    None (the baseline then runs torch's silu and mul, two kernels)."""
+    try:
+        import vllm._C  # noqa: F401
+        import torch
+
+        op = torch.ops._C.silu_and_mul
+        return lambda out, x: op(out, x), "vllm silu_and_mul"
+    except Exception:
+        return None, None
+
+
+def cublas_step_fn(kind, act, t, variant="eager"):
+    """The unfused path as a zero-argument callable.
+    eager: torch.matmul (cuBLAS) GEMM -> separate activation / gate kernels -> GEMM.
+    fused_epilogue: production layout -- standard FFN: cuBLASLt GEMM with the ReLU /
+      GELU epilogue (torch._addmm_activation) -> GEMM; gated FFN: one GEMM over the packed
+      [K, 2N] gate|up weight -> one fused SwiGLU kernel -> GEMM."""
     import torch
 
     f = torch.nn.functional
+    if variant == "eager":
+        if kind == "gated_ffn":
+            def fn():
+                return (f.silu(t["A"] @ t["B0"]) * (t["A"] @ t["B1"])) @ t["D"]
+        else:
+            actf = {"relu": torch.relu, "silu": f.silu, "gelu": lambda x: f.gelu(x, approximate="tanh"),
+                    "identity": lambda x: x}[act]
+
+            def fn():
+                return actf(t["A"] @ t["B"]) @ t["D"]
+        return fn, "torch.matmul (cuBLAS) + separate elementwise activation kernels"
+    m, k = t["A"].shape
+    n = t["D"].shape[0]
     if kind == "gated_ffn":
-        def fn():
-            return (f.silu(t["A"] @ t["B0"]) * (t["A"] @ t["B1"])) @ t["D"]
-    else:
-        actf = {"relu": torch.relu, "silu": f.silu, "gelu": lambda x: f.gelu(x, approximate="tanh"),
-                "identity": lambda x: x}[act]
+        w = torch.cat([t["B0"], t["B1"]], dim=1).contiguous()  # [K, 2N] packed gate|up
+        h = torch.empty((m, 2 * n), dtype=t["A"].dtype, device=t["A"].device)
+        c = torch.empty((m, n), dtype=t["A"].dtype, device=t["A"].device)
+        op, op_name = _silu_and_mul()
 
         def fn():
-            return actf(t["A"] @ t["B"]) @ t["D"]
-    for _ in range(3):
-        fn()
-    times = time_steps(fn, steps, flush, stream)
-    ms = float(np.median(times))
+            torch.matmul(t["A"], w, out=h)
+            if op is not None:
+                op(c, h)
+                return c @ t["D"]
+            return (f.silu(h[:, :n]) * h[:, n:]) @ t["D"]
+        return fn, f"packed gate|up GEMM [K,2N] -> {op_name or 'torch silu*mul'} -> GEMM"
+    zero = torch.zeros(n, dtype=t["A"].dtype, device=t["A"].device)
+    if act in ("relu", "gelu"):
+        gelu = act == "gelu"
+
+        def fn():
+            return torch._addmm_activation(zero, t["A"], t["B"], use_gelu=gelu) @ t["D"]
+        return fn, f"cuBLASLt GEMM with fused {act.upper()} epilogue -> GEMM"
+    return cublas_step_fn(kind, act, t, "eager")
+
+
+def cublas_unfused(kind, act, t, flush, stream, steps):
+    """Unfused cuBLAS baselines, each timed eagerly and as a replayed CUDA graph
+    (host launch cost removed); `best` is the fastest of all."""
+    import torch
+
     m, k = t["A"].shape
     n, l = t["D"].shape
     fl = flops_of(kind, m, n, k, l)
-    return {"ms": round(ms, 4), "tflops": round(fl / (ms * 1e-3) / 1e12, 2),
-            "path": "torch.matmul (cuBLAS) + elementwise act, 3-4 kernels"}
+    variants = {}
+    for variant in ("eager", "fused_epilogue"):
+        fn, path = cublas_step_fn(kind, act, t, variant)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ms = float(np.median(time_steps(fn, steps, flush, stream)))
+        variants[variant] = {"ms": round(ms, 4), "tflops": round(fl / (ms * 1e-3) / 1e12, 2), "path": path}
+        try:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                fn()
+                with torch.cuda.graph(g, stream=s):
+                    fn()
+            torch.cuda.current_stream().wait_stream(s)
+            torch.cuda.synchronize()
+            gms = float(np.median(time_steps(g.replay, steps, flush, stream)))
+            variants[variant + "_graph"] = {"ms": round(gms, 4), "tflops": round(fl / (gms * 1e-3) / 1e12, 2),
+                                            "path": path + " (CUDA graph)"}
+        except Exception as exc:  # informative only
+            variants[variant + "_graph"] = {"error": repr(exc)}
+    best = min((v["ms"], key) for key, v in variants.items() if "ms" in v)
+    return {"best_ms": best[0], "best": best[1], "variants": variants}
 
 
 def load_ncu_summary(name):
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    """ncu DRAM bytes per launch (profiles/r02/dram_summary.json, written from
+    tools/dram_bytes.py captures on the B200)."""
+    path = os.path.join(ROOT, "profiles", "r02", "dram_summary.json")
     if not os.path.exists(path):
         return {}
     with open(path) as fh:
         doc = json.load(fh)
-    entry = doc.get(name, {})
-    entry = dict(entry)
-    entry["source"] = f"profiles/ncu_summary.json ({doc.get('round', '?')})"
+    entry = dict(doc.get(name, {}))
+    entry["source"] = f"profiles/r02/dram_summary.json ({doc.get('method', '?')})"
     return entry
 
 
 def run_reference(args, rank, world):
-    """Reference arm: the reference's CPU path (oracle port) on this host, rank 0 only."""
+    """Reference arm: the reference's own CPU execution path (fuseplan.simulator.
+    execute_plan from baseline/_ref, numpy BLAS with all host threads) on this host,
+    rank 0 only; each step one plan-faithful execution of a token-row sample."""
     if rank != 0:
         return None
     kind, act, m, n, k, l, desc = WORKLOADS[args.workload]
-    import oracle
-
     # all host threads for the BLAS (torchrun exports OMP_NUM_THREADS=1 to every rank)
     try:
         from threadpoolctl import threadpool_limits
@@ -602,25 +778,20 @@ def run_reference(args, rank, world):
         threadpool_limits(limits=len(os.sched_getaffinity(0)))
     except Exception:
         pass
-
-    # each step = one plan-faithful replay of a token-row sample of the chain,
-    # sized so the whole --steps K --warmup W run stays within ~2 minutes
-    plan_full = _reference_plan(args.workload)
     probe_rows = min(m, 64)
-    probe_in = oracle.make_inputs(kind, probe_rows, n, k, l, seed=0, dtype=np.float32)
+    probe, _, _ = reference_cpu_step(args.workload, probe_rows)
     t0 = time.perf_counter()
-    cpu_reference_step(kind, act, probe_rows, n, k, l, probe_in, _rows_plan(plan_full, probe_rows))
+    probe()
     per_row = (time.perf_counter() - t0) / probe_rows
-    budget = 120.0 / max(1, args.steps + args.warmup)
+    budget = 120.0 / max(1, args.steps + args.warmup)  # whole --steps K --warmup W run within ~2 minutes
     rows = int(min(m, max(64, budget / max(per_row, 1e-9))) // 64 * 64)
-    plan_doc = _rows_plan(plan_full, rows)
-    inputs = oracle.make_inputs(kind, rows, n, k, l, seed=0, dtype=np.float32)
+    step, cpu_kind, path = reference_cpu_step(args.workload, rows)
     for _ in range(args.warmup):
-        cpu_reference_step(kind, act, rows, n, k, l, inputs, plan_doc)
+        step()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        cpu_reference_step(kind, act, rows, n, k, l, inputs, plan_doc)
+        step()
         times.append(time.perf_counter() - t0)
     total = float(sum(times))
     fl = flops_of(kind, rows, n, k, l)
@@ -632,17 +803,16 @@ def run_reference(args, rank, world):
         "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic U[-1,1] f32 (seeded)",
         "config": {"workload": desc, "m_per_gpu": m, "n": n, "k": k, "l": l, "kind": kind, "activation": act,
-                   "path": "oracle.replay_plan: numpy restatement of fuseplan simulator.execute_plan "
-                           "(the reference's CPU execution path), reference top-1 plan"},
-        "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} steps, each one plan-faithful replay of a {rows}-of-{m} "
+                   "path": path + ", reference search top-1 plan"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "TFLOP/s", "cores": cores, "kind": cpu_kind,
+                         "sample": f"{args.steps} steps, each one plan-faithful execution of a {rows}-of-{m} "
                                    f"token-row sample of the chain (n={n} k={k} l={l})"},
         "e2e": {"value": round(value, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
 def run_extra(args):
-    """Other BASELINE configs, single GPU, fused vs cuBLAS (informative)."""
+    """Other BASELINE configs, single GPU, fused vs cuBLAS (same method as the headline)."""
     import torch
 
     from paper_2512_12949_b200 import runtime
@@ -660,16 +830,18 @@ def run_extra(args):
         try:
             graph = graph_of(name)
             t = make_device_inputs(kind, m, n, k, l, 7, "cuda")
-            cfg, cfg_name, _ = choose_config(name, t)
+            cfg, cfg_name, plan, _ = choose_config(name, t, flush=flush)
             o = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
             fn = lambda: runtime.launch(graph, cfg, t, out=o)  # noqa: E731
             for _ in range(3):
                 fn()
-            ms = float(np.median(time_steps(fn, 5, flush, torch.cuda.current_stream())))
+            ms = float(np.median(time_steps(fn, 20, flush, torch.cuda.current_stream())))
             fl = flops_of(kind, m, n, k, l)
+            cub = cublas_unfused(kind, act, t, flush, torch.cuda.current_stream(), 20)
             out[name] = {"workload": desc, "fused_ms": round(ms, 4), "fused_tflops": round(fl / ms / 1e9, 1),
-                         "launch": cfg.as_dict(), "plan": cfg_name,
-                         "cublas_unfused": cublas_unfused(kind, act, t, flush, torch.cuda.current_stream(), 5)}
+                         "cublas_best_ms": cub["best_ms"], "speedup_vs_cublas_best": round(cub["best_ms"] / ms, 4),
+                         "launch": cfg.as_dict(), "plan": cfg_name, "cublas_unfused": cub,
+                         "hbm": hbm_table(name, plan)}
         except Exception as exc:  # informative only
             out[name] = {"error": repr(exc)}
     return out

@@ -93,9 +93,7 @@ typedef struct ffKernelConfig {
   int32_t steps;       /* derived: n-steps per split */
   int32_t units;       /* derived: m_tiles * l_clusters * n_splits work units */
   int32_t rings;       /* derived: co-resident rings launched (persistent over units) */
-  int32_t grid_ctas;   /* derived: CTAs launched (rings * ring * CTAs per member, + 2 * helpers) */
-  int32_t helpers;     /* derived (pair kernel): helper CTA pairs on the SMs the rings leave idle */
-  int32_t helper_x;    /* derived (pair kernel): last hops of every member n-step run by the helpers */
+  int32_t grid_ctas;   /* derived: CTAs launched (rings * ring * CTAs per member) */
 } ffKernelConfig;
 
 /* Tensors: row-major, the reference layouts (simulator.py:112-123):
@@ -162,7 +160,11 @@ size_t ff_chain_workspace_bytes(const ffChainDesc* chain, const ffKernelConfig* 
 int ff_chain_launch(const ffChainDesc* chain, const ffKernelConfig* cfg, const ffTensors* t, void* workspace,
                     size_t workspace_bytes, void* stream);
 
-/* Lower + launch in one call: the drop-in for simulator.execute_plan. */
+/* Lower + launch in one call: the drop-in for simulator.execute_plan.  The plan
+ * is lowered under the first transport that executes it (CTA pairs, then the
+ * 1-CTA L2 and DSM kernels); ff_plan_workspace_bytes sizes its workspace
+ * (0 when the plan has no lowering: ff_chain_run_plan then reports why). */
+size_t ff_plan_workspace_bytes(const ffChainDesc* chain, const ffPlanDesc* plan);
 int ff_chain_run_plan(const ffChainDesc* chain, const ffPlanDesc* plan, const ffTensors* t, void* workspace,
                       size_t workspace_bytes, void* stream);
 
@@ -177,6 +179,17 @@ int ff_chain_kernel_count(const ffChainDesc* chain, const ffKernelConfig* cfg);
  * per-CTA wait-cycle counters (slots 0-15) and globaltimer stamps (16-31) on
  * every launch (NULL disables; default). */
 void ff_set_profile_buffer(void* dev_ptr);
+
+/* Kernel-variant selection (process-wide; default 0 = the tuned kernels), for
+ * A/B measurements and the tests that pin every variant against the oracle. */
+#define FF_VARIANT_NO_KROT 0x1u          /* common GEMM0 k order in every ring member */
+#define FF_VARIANT_NO_QUAD 0x2u          /* plain CTA pairs, no weight-multicast quads */
+#define FF_VARIANT_FORCE_QUAD 0x4u       /* quads whenever they can launch */
+#define FF_VARIANT_FINISH_REGIONS 0x8u   /* 1-CTA kernels: split-N finish through exchange regions */
+#define FF_VARIANT_WEIGHTS_EVICT_FIRST 0x10u /* pair kernel: weight tiles + prefetches with L2 evict_first */
+#define FF_VARIANT_SCRATCH_NORMAL 0x20u      /* pair kernel: C exchange scratch with the default L2 priority */
+#define FF_VARIANT_WEIGHTS_EVICT_LAST 0x40u  /* pair kernel: weight tiles + prefetches with L2 evict_last */
+void ff_set_variant(uint32_t flags);
 
 /* Thread-local message for the last non-OK status. */
 const char* ff_last_error(void);

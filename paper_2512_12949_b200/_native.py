@@ -38,9 +38,11 @@ EXPORTS = (
     "ff_chain_workspace_bytes",
     "ff_chain_launch",
     "ff_chain_run_plan",
+    "ff_plan_workspace_bytes",
     "ff_chain_launch_debug",
     "ff_chain_kernel_count",
     "ff_set_profile_buffer",
+    "ff_set_variant",
     "ff_last_error",
     "ff_version",
     "ff_conv_chain_desc",
@@ -99,8 +101,6 @@ class KernelConfig(ctypes.Structure):
         ("units", ctypes.c_int32),
         ("rings", ctypes.c_int32),
         ("grid_ctas", ctypes.c_int32),
-        ("helpers", ctypes.c_int32),
-        ("helper_x", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -150,10 +150,13 @@ def load(path: str = LIB_PATH):
                                         ctypes.c_size_t, ctypes.c_void_p]
         lib.ff_chain_run_plan.argtypes = [P(ChainDesc), P(PlanDesc), P(Tensors), ctypes.c_void_p,
                                           ctypes.c_size_t, ctypes.c_void_p]
+        lib.ff_plan_workspace_bytes.argtypes = [P(ChainDesc), P(PlanDesc)]
+        lib.ff_plan_workspace_bytes.restype = ctypes.c_size_t
         lib.ff_chain_launch_debug.argtypes = [P(ChainDesc), P(KernelConfig), P(Tensors), ctypes.c_void_p,
                                               ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]
         lib.ff_chain_kernel_count.argtypes = [P(ChainDesc), P(KernelConfig)]
         lib.ff_set_profile_buffer.argtypes = [ctypes.c_void_p]
+        lib.ff_set_variant.argtypes = [ctypes.c_uint32]
         lib.ff_conv_chain_desc.argtypes = [P(ConvDesc), P(ChainDesc)]
         lib.ff_conv_chain_lower.argtypes = [P(ConvDesc), ctypes.c_int32, ctypes.c_int32, P(KernelConfig)]
         lib.ff_conv_chain_workspace_bytes.argtypes = [P(ConvDesc), P(KernelConfig)]
@@ -174,7 +177,12 @@ def check(rc: int) -> None:
     if rc == FF_ERR_PLAN:
         raise PlanError(msg)
     if rc == FF_ERR_CAPACITY:
-        raise CapacityExceeded("C", "dsm", 0)
+        # the library reports "<tensor>:<floor tier>:<unplaced bytes>|<text>" (ff_chain.cu: fail_capacity)
+        head, _, text = msg.partition("|")
+        tensor, floor, unplaced = (head.split(":") + ["", "", "0"])[:3]
+        exc = CapacityExceeded(tensor or "C", floor or "tmem", int(unplaced) if unplaced.isdigit() else 0)
+        exc.args = (f"{exc.args[0]} ({text})",) if text else exc.args
+        raise exc
     if rc == FF_ERR_UNSUPPORTED:
         raise UnsupportedPlan(msg)
     raise NativeError(f"native status {rc}: {msg}")

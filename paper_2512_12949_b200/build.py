@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libff_chain.so")
-SOURCES = ("ff_chain.cu", "dsm_bench.cu", "dsm_primitives.cu")
+SOURCES = ("ff_chain.cu", "dsm_primitives.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

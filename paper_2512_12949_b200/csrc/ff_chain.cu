@@ -24,6 +24,12 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+// CapacityExceeded (errors.py:32-45): `tensor` does not fit at or above tier `floor`
+// by `unplaced` bytes; the Python binding rebuilds the exception from this text.
+int fail_capacity(const char* tensor, const char* floor, long long unplaced, const std::string& msg) {
+  return fail(FF_ERR_CAPACITY, std::string(tensor) + ":" + floor + ":" + std::to_string(unplaced) + "|" + msg);
+}
+
 CUtensorMapDataType elem_type(const ffChainDesc* ch) {
   return ch->dtype == FF_DTYPE_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
 }
@@ -130,14 +136,65 @@ bool make_map_nd(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void*
          CUDA_SUCCESS;
 }
 
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
+// SM count of the current device (cached per device ordinal).
 int num_sms_cached() {
-  static int n = -1;
-  if (n < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  static std::atomic<int> n[kMaxDevices];
+  const int dev = current_device();
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n;
+  return v;
+}
+
+// One-time per-(kernel, device) function attributes: attributes apply to the
+// current device only, so a process that launches on several GPUs sets them on
+// each.  Returns the first error (sticky per device).
+template <typename Fn>
+cudaError_t once_per_device(std::once_flag (&flags)[kMaxDevices], cudaError_t (&errs)[kMaxDevices], Fn fn) {
+  const int dev = current_device();
+  std::call_once(flags[dev], [&] { errs[dev] = fn(); });
+  return errs[dev];
+}
+
+// Launches that spin on other CTAs' flags need the whole grid co-resident: they
+// are cooperative.  A profiler that replays kernels (ncu) cannot replay a
+// cooperative cluster launch, so with one attached (CUDA_INJECTION64_PATH, or
+// FF_NO_COOPERATIVE=1) the attribute is dropped; the grid is sized to
+// co-residency either way and a replaying profiler runs one kernel at a time.
+bool profiler_attached() {
+  for (const char* v : {"CUDA_INJECTION64_PATH", "NSIGHT_COMPUTE_HOST_PORT", "NV_COMPUTE_PROFILER_PERFWORKS_DIR"})
+    if (std::getenv(v) != nullptr) return true;
+  const char* pre = std::getenv("LD_PRELOAD");
+  return pre != nullptr && (std::strstr(pre, "nsight") || std::strstr(pre, "Injection") || std::strstr(pre, "ncu"));
+}
+bool cooperative_allowed() {
+  static const bool ok = std::getenv("FF_NO_COOPERATIVE") == nullptr && !profiler_attached();
+  return ok;
+}
+
+// Launch with the cooperative attribute (the last of `attrs`); only a device or
+// driver without cooperative support (cudaErrorNotSupported) gets a plain
+// launch -- every other refusal, e.g. a grid too large to be co-resident, fails.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(cudaLaunchConfig_t& lc, void (*kern)(KArgs...), Args&&... args) {
+  if (!cooperative_allowed()) lc.numAttrs -= 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, kern, args...);
+  if (e == cudaErrorNotSupported && cooperative_allowed()) {
+    cudaGetLastError();
+    lc.numAttrs -= 1;
+    e = cudaLaunchKernelEx(&lc, kern, args...);
+  }
+  return e;
 }
 
 // ---------------------------------------------------------------------------
@@ -153,7 +210,9 @@ struct StagesFor {
 };
 
 // Co-resident clusters of a given size on a 148-SM B200 with ~225 KB smem per
-// CTA (cudaOccupancyMaxActiveClusters, profiles/r01/dsm_bandwidth.log).
+// CTA (cudaOccupancyMaxActiveClusters, profiles/r01/dsm_bandwidth.log): the
+// offline estimate used by the lowering (no device needed); launches clamp to
+// the occupancy API's answer for the actual kernel and device.
 int table_active_clusters(int cluster, int num_sms) {
   int n;
   switch (cluster) {
@@ -168,7 +227,7 @@ int table_active_clusters(int cluster, int num_sms) {
 }
 
 struct WsLayout {
-  size_t e_off, c_off, f_off, n_off, s_off, h_off, total;
+  size_t e_off, c_off, f_off, n_off, s_off, total;
   bool e_memset;  // fp32 E larger than the zero zone: clear it before the launch
 };
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -180,9 +239,23 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // (split_finish), and no config puts C scratch inside them, so a workspace
 // zero-filled once stays valid whatever configs share it.  A split chain whose
 // fp32 E exceeds the zone spills past it and clears it with a memset first.
+// flag region (u32 words): [0, 2^17) ring chunk-ready flags, [2^17, 2^18) split-N slab
+// flags; its last word holds the device epoch
 constexpr size_t kFlagBytes = 1u << 20;
+constexpr size_t kRingFlagBytes = 512u << 10;
 constexpr size_t kCntBytes = 256u << 10;
 constexpr size_t kEZoneBytes = 32u << 20;
+// Pair kernel: N not a whole number of ring steps per split (ragged last n-step).
+bool pair_ragged(const ffChainDesc* ch, const ffKernelConfig* c) {
+  return ch->n != (int64_t)c->n_splits * c->steps * c->ring * c->nb;
+}
+// Pair kernel, non-ragged: C exchange slots per ring member.  A ring that runs more
+// n-steps than slots reuses them every 3 steps (the kernel's c_row / wait_slot_free);
+// one unit per ring keeps one slot per step.
+int pair_c_slots(const ffKernelConfig* c) {
+  return c->units > c->rings ? 3 : std::min(3, std::max(1, (int)c->steps));
+}
+
 WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = false) {
   WsLayout w{};
   const bool pair = c->exchange == FF_XCHG_L2_PAIR;
@@ -201,20 +274,22 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   // (a gated ring-1 split config once put its exchange regions there)
   size_t off = w.e_off + std::max(e_bytes, kEZoneBytes);
   w.c_off = off;
-  if (c_scratch) off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
+  if (c_scratch) {
+    if (pair && !pair_ragged(ch, c))  // per-(ring, member, slot) regions of 256 rows x nb columns
+      off = align256(off + (size_t)c->rings * c->ring * pair_c_slots(c) * 256 * c->nb * 2);
+    else  // the whole intermediate
+      off = align256(off + (size_t)c->m_tiles * (pair ? 256 : 128) * ch->n * 2);
+  }
   // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
   w.s_off = off;
   if (c->n_splits > 1)  // split-N exchange regions (pair kernel, and the 1-CTA kernels' final units)
     off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * (pair ? 256 : 128) * ch->l * sizeof(float));
-  // helper pairs' E partials, one region per (E tile, n-step); plain stores, no zero invariant
-  w.h_off = off;
-  if (pair && c->helpers > 0) off = align256(off + (size_t)c->steps * c->m_tiles * 256 * ch->l * sizeof(float));
   w.total = off;
   return w;
 }
 
 unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
-uint32_t g_dbg = 0;  // diagnostics: ff_set_debug_mode
+uint32_t g_variant = 0;  // kernel-variant selection for A/B runs and tests (ff_set_variant, FF_VARIANT_*)
 
 // Split-N finish by exchange regions (pair kernel): one unit per ring, S | 128
 // with 8-row slices, and the slab flags of every E tile fit their region.
@@ -222,38 +297,6 @@ bool pair_finish_regions(const ffChainDesc* ch, const ffKernelConfig* c, int rin
   return c->n_splits > 1 && c->n_splits <= 8 && c->units <= rings && 128 % c->n_splits == 0 &&
          (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 < (1u << 17);
 }
-
-// Helper pairs (pair kernel) on the SMs a split-N launch leaves idle: they take
-// the last x hops of every member n-step.  x balances the members' work
-// (steps GEMM0 chunks of r hop-times each + steps*(G-x) hops) against the
-// helpers' (about one chunk of r hop-times waiting for the first published C,
-// then steps*units*G*x/H hops); the NS = m_tiles*G*steps segments are dealt out
-// in contiguous blocks.  Two n-steps at most: the helper zone then
-// sums two partials into zero, which is order-independent.
-void plan_helpers(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
-  c->helpers = 0;
-  c->helper_x = 0;
-  // Opt-in (measured slower, profiles/r01/helper_x.log): the fused chain at 128 SMs is
-  // already bound by the chip's aggregate operand feed; the helpers' extra hops slow
-  // the members' hops by as much as they add.  FF_HELPERS=1 or debug bit 26 enables.
-  static const bool env_on = std::getenv("FF_HELPERS") != nullptr;
-  if (c->exchange != FF_XCHG_L2_PAIR || (g_dbg & (1u << 24)) || !(env_on || (g_dbg & (1u << 26)))) return;
-  if (!pair_finish_regions(ch, c, c->rings) || c->steps > 2 || c->l_clusters != 1) return;
-  if (ch->n != (int64_t)c->n_splits * c->steps * c->ring * c->nb) return;  // ragged n-steps
-  const int H = (num_sms - c->rings * c->ring * 2) / 2;
-  if (H < 1) return;
-  const double r = (double)ch->k / (ch->kind == FF_KIND_GATED ? 128 : 256);
-  const double G = c->ring, st = c->steps, units = c->units;
-  // members: st*r + st*(G - x) hop-times; helpers: r + 2 (first chunks drained and
-  // published) + st*x*units*G/H
-  int x = (int)std::lround((st * r + st * G - r - 2) / (st * (1.0 + units * G / H)));
-  if ((g_dbg >> 16) & 15u) x = (int)((g_dbg >> 16) & 15u) - 1;
-  x = std::min(x, c->ring - 2);
-  if (x < 1) return;
-  c->helpers = H;
-  c->helper_x = x;
-}
-
 
 template <bool kGated, int kNB, int kLB, int kMode>
 int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensors* t, void* ws,
@@ -263,12 +306,13 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   using C = ff::ChainCfg<kGated, kNB, kLB, kStages, kMode>;
   auto kern = ff::ff_chain_kernel<kGated, kNB, kLB, kStages, kMode>;
 
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM);
-    if (attr_err == cudaSuccess && kMode == ff::XCHG_DSM)
-      attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t errs[kMaxDevices];
+  const cudaError_t attr_err = once_per_device(once, errs, [&] {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM);
+    if (r == cudaSuccess && kMode == ff::XCHG_DSM)
+      r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return r;
   });
   if (attr_err != cudaSuccess)
     return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
@@ -332,28 +376,36 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   lc.blockDim = dim3(256, 1, 1);
   lc.dynamicSmemBytes = C::kSMEM;
   lc.stream = stream;
-  cudaLaunchAttribute attr[1];
+  // Every launch is cooperative: ring members spin on each other's flags (L2
+  // transport), split contributors on each other's arrivals (shared finish, exchange
+  // regions), so the whole grid must be co-resident.  DSM rings are clusters.
+  cudaLaunchAttribute attr[2];
+  int nattr = 0;
   int rings;
   if (kMode == ff::XCHG_DSM) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cfg->ring;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    attr[nattr].id = cudaLaunchAttributeClusterDimension;
+    attr[nattr].val.clusterDim.x = cfg->ring;
+    attr[nattr].val.clusterDim.y = 1;
+    attr[nattr].val.clusterDim.z = 1;
+    ++nattr;
     lc.gridDim = dim3(cfg->ring, 1, 1);
     lc.attrs = attr;
-    lc.numAttrs = 1;
+    lc.numAttrs = nattr;
     int active = 0;
-    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0)
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0) {
+      cudaGetLastError();
       active = table_active_clusters(cfg->ring, num_sms_cached());
+    }
     rings = std::min(cfg->units, active);
   } else {
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    lc.attrs = attr;
-    lc.numAttrs = 1;
     rings = std::min(cfg->units, num_sms_cached() / cfg->ring);
     if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring larger than the number of SMs");
   }
+  attr[nattr].id = cudaLaunchAttributeCooperative;
+  attr[nattr].val.cooperative = 1;
+  ++nattr;
+  lc.attrs = attr;
+  lc.numAttrs = nattr;
   lc.gridDim = dim3(rings * cfg->ring, 1, 1);
 
   ff::ChainArgs a{};
@@ -369,7 +421,6 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.n_units = cfg->units;
   a.n_rings = rings;
   a.act = ch->activation;
-  a.epoch = 0;
   a.dev_epoch = reinterpret_cast<uint32_t*>(wsb + wl.f_off) + (kFlagBytes / 4 - 1);  // last flag-region word
   a.exit_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off) + (kCntBytes / 4 - 1);    // last counter word
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
@@ -378,11 +429,10 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.tile_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
-  a.dbg = g_dbg;
   a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
-  a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
+  a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;
   a.slab = reinterpret_cast<float*>(wsb + wl.s_off);
-  // final-unit split-N reduce-scatter through exchange regions (debug bit 29, opt-in): one
+  // final-unit split-N reduce-scatter through exchange regions (FF_VARIANT_FINISH_REGIONS, opt-in): one
   // unit per ring, 8-row slices, the S slots (the whole fp32 tile) in the drained stages
   // and the bf16 row slice in the own slot.  Measured slower than the TMA reduce-add +
   // last-arriver finish for GPT-2s (29.7 vs 26.6 us, profiles/r01/timeline_gpt2s_regions.log):
@@ -390,7 +440,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   // region path adds the partner loads
   a.finish_tma = S > 1 && S <= 8 && 128 % S == 0 && R % 8 == 0 && cfg->units <= rings && !conv2 &&
                  (size_t)128 * kLB * 4 <= (size_t)C::kOFF_OWN && (size_t)R * kLB * 2 <= (size_t)C::kCHUNK_BYTES &&
-                 (size_t)cfg->m_tiles * (L / kLB) * 16 < (1u << 17) && (g_dbg & (1u << 29));
+                 (size_t)cfg->m_tiles * (L / kLB) * 16 < (1u << 17) && (g_variant & FF_VARIANT_FINISH_REGIONS);
   if (implicit || conv2) {
     a.conv_k1 = implicit ? conv->k1 : 0;
     a.conv_H = conv->h;
@@ -404,7 +454,7 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, mA, mB0, mB1, mD, mC, mCs, mE, mW, mSlab, mEr, a);
+  cudaError_t e = launch_coop(lc, kern, mA, mB0, mB1, mD, mC, mCs, mE, mW, mSlab, mEr, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx: ") + cudaGetErrorString(e));
 
   return FF_OK;
@@ -425,9 +475,31 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
   using C = ff::PairCfg<kGated, 256, kStages>;
   auto kern = ff::ff_chain_pair_kernel<kGated, 256, kStages, kPacked, kQuad, kRagged>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM); });
+  static std::once_flag once[kMaxDevices];
+  static cudaError_t errs[kMaxDevices];
+  static int max_clusters[kMaxDevices];  // co-resident clusters of this kernel (occupancy API), per device
+  const cudaError_t attr_err = once_per_device(once, errs, [&] {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSMEM);
+    if (r != cudaSuccess) return r;
+    cudaLaunchConfig_t probe = {};
+    cudaLaunchAttribute cl[1];
+    cl[0].id = cudaLaunchAttributeClusterDimension;
+    cl[0].val.clusterDim.x = kQuad ? 4 : 2;
+    cl[0].val.clusterDim.y = 1;
+    cl[0].val.clusterDim.z = 1;
+    probe.gridDim = dim3(kQuad ? 4 : 2, 1, 1);
+    probe.blockDim = dim3(256, 1, 1);
+    probe.dynamicSmemBytes = C::kSMEM;
+    probe.attrs = cl;
+    probe.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &probe) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = kQuad ? table_active_clusters(4, num_sms_cached()) : num_sms_cached() / 2;
+    }
+    max_clusters[current_device()] = n;
+    return cudaSuccess;
+  });
   if (attr_err != cudaSuccess)
     return fail(FF_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
@@ -498,9 +570,12 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.d, BF, 3, t->d, d, st, b);
   }
-  {  // C scratch [mpad][N] as {64, mpad, N/64}
+  {  // C exchange scratch: regions [rings*G*slots][256 rows][nb] as {64, regions*256, nb/64}
+     // (ragged: the whole intermediate [mpad][N] as {64, mpad, N/64})
     const bool l2x = cfg->ring > 1 || !kGated;
-    const uint64_t d[3] = {64, l2x ? mpad : M, l2x ? N / 64 : K / 64}, st[2] = {(l2x ? N : K) * 2, 128};
+    const uint64_t rows = kRagged ? mpad : (uint64_t)cfg->rings * cfg->ring * pair_c_slots(cfg) * 256;
+    const uint64_t cols = kRagged ? N : (uint64_t)C::kN0;
+    const uint64_t d[3] = {64, l2x ? rows : M, l2x ? cols / 64 : K / 64}, st[2] = {(l2x ? cols : K) * 2, 128};
     const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.c, BF, 3, l2x ? (const void*)(wsb + wl.c_off) : t->a, d, st, b);
   }
@@ -547,11 +622,14 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   if (!ok) return fail(FF_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment or driver entry point)");
 
   if (cfg->ring > 64) return fail(FF_ERR_UNSUPPORTED, "ring of more than 64 pairs");
-  int rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
-  if (kQuad) {  // rings in X/Y couples, clusters of 4 co-resident
-    rings = std::min(rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring));
-    rings &= ~1;
-  }
+  // co-resident rings: pairs the occupancy API guarantees for this kernel on this device
+  const int pairs = max_clusters[current_device()] * (kQuad ? 2 : 1);
+  int rings = std::min(cfg->units, pairs / cfg->ring);
+  if (kQuad) rings &= ~1;  // rings in X/Y couples
+  // the C scratch is laid out for cfg->rings rings; fewer co-resident rings than
+  // planned (another tenant's occupancy) may need slot reuse the layout lacks
+  if (!kRagged && rings < cfg->units && pair_c_slots(cfg) < 3)
+    return fail(FF_ERR_UNSUPPORTED, "fewer co-resident CTA pairs than the launch was planned for");
   if (rings < 1) return fail(FF_ERR_UNSUPPORTED, "ring of pairs larger than the GPU");
   ff::ChainArgs a{};
   a.M = (int)M;
@@ -568,7 +646,6 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.n_units = cfg->units;
   a.n_rings = rings;
   a.act = ch->activation;
-  a.epoch = 0;
   a.dev_epoch = reinterpret_cast<uint32_t*>(wsb + wl.f_off) + (kFlagBytes / 4 - 1);  // last flag-region word
   a.exit_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off) + (kCntBytes / 4 - 1);    // last counter word
   a.E = reinterpret_cast<__nv_bfloat16*>(t->e);
@@ -578,7 +655,6 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.slab = reinterpret_cast<float*>(wsb + wl.s_off);
   a.c_debug = reinterpret_cast<__nv_bfloat16*>(c_debug);
   a.prof = g_prof;
-  a.dbg = g_dbg;
   a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   // hops deferred past GEMM0(T+1): about one C drain (+ its store for the
   // standard FFN, whose hop 0 reads the own chunk back from L2) worth of MMA
@@ -588,23 +664,26 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.defer = cfg->ring - 1;
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
   a.finish_tma = pair_finish_regions(ch, cfg, rings);
-  // helper pairs (planned by finish_config for the non-quad launch)
-  a.helpers = (!kQuad && rings == cfg->rings) ? cfg->helpers : 0;
-  a.helper_x = a.helpers > 0 ? cfg->helper_x : 0;
-  a.hzone = reinterpret_cast<float*>(wsb + wl.h_off);
-  if ((g_dbg >> 8) & 15u) a.defer = std::min(cfg->ring - 1, (int)((g_dbg >> 8) & 15u) - 1);
   a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
   // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
-  // debug bit 27 restores the common order
-  a.krot = (g_dbg & (1u << 27)) ? 0 : 1;
-  a.defer_last = (g_dbg & 128u) ? 0 : 1;
-  if ((g_dbg >> 12) & 15u) a.prefetch = (int)((g_dbg >> 12) & 15u) - 1;
+  // FF_VARIANT_NO_KROT restores the common order
+  a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;
+  a.defer_last = 1;
+  a.c_slots = kRagged ? 0 : pair_c_slots(cfg);
+  // L2 policies (A/B timelines in profiles/r02/l2_policy_ab.log): the C exchange scratch
+  // is evict_last (GPT-6.7B -1.1 us, LLaMA-1B -1.3 us); weights keep the default
+  // priority (evict_first made GPT-6.7B 6 % slower: the prefetched lines were evicted
+  // before their TMA loads) unless a variant asks otherwise
+  a.wpolicy = (g_variant & FF_VARIANT_WEIGHTS_EVICT_FIRST) ? ff::L2_EVICT_FIRST
+              : (g_variant & FF_VARIANT_WEIGHTS_EVICT_LAST) ? ff::L2_EVICT_LAST
+                                                            : ff::L2_NORMAL;
+  a.cpolicy = (g_variant & FF_VARIANT_SCRATCH_NORMAL) ? ff::L2_NORMAL : ff::L2_EVICT_LAST;
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
   }
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3(rings * cfg->ring * 2 + 2 * a.helpers, 1, 1);
+  lc.gridDim = dim3(rings * cfg->ring * 2, 1, 1);
   lc.blockDim = dim3(256, 1, 1);
   lc.dynamicSmemBytes = C::kSMEM;
   lc.stream = stream;
@@ -616,18 +695,8 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   attr[1].id = cudaLaunchAttributeCooperative;
   attr[1].val.cooperative = 1;
   lc.attrs = attr;
-  // Cooperative + cluster guarantees co-residency of the rings; ncu cannot
-  // replay that combination, so FF_NO_COOPERATIVE=1 (profiling) or debug bit2
-  // drops the cooperative attribute (the grid is sized to fit either way).
-  static const bool no_coop = std::getenv("FF_NO_COOPERATIVE") != nullptr;
-  lc.numAttrs = ((g_dbg & 4u) || no_coop) ? 1 : 2;
-  cudaError_t e = cudaLaunchKernelEx(&lc, kern, maps, a);
-  if (e != cudaSuccess) {
-    // cooperative + cluster not accepted: the grid is sized to co-residency anyway
-    cudaGetLastError();
-    lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, kern, maps, a);
-  }
+  lc.numAttrs = 2;  // cooperative + cluster: the rings spin on each other's flags (launch_coop)
+  cudaError_t e = launch_coop(lc, kern, maps, a);
   if (e != cudaSuccess) return fail(FF_ERR_CUDA, std::string("cudaLaunchKernelEx(pair): ") + cudaGetErrorString(e));
   return FF_OK;
 }
@@ -636,13 +705,12 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
 // share their weights: an even number of m tiles, an even number of rings of
 // at most one unit each... any even ring count works (units 2j / 2j+1 pair up).
 bool quad_ok(const ffKernelConfig* cfg, bool gated) {
-  if (g_dbg & 64u) return false;  // diagnostics: force the plain pair kernel
-  if (cfg->helpers > 0) return false;  // helper pairs fill the SMs a cluster-of-4 launch cannot
+  if (g_variant & FF_VARIANT_NO_QUAD) return false;  // A/B and tests: force the plain pair kernel
   if (cfg->m_tiles % 2 || cfg->units % 2) return false;
   const int pair_rings = std::min(cfg->units, num_sms_cached() / (2 * cfg->ring));
   int rings = std::min(pair_rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring)) & ~1;
   if (rings < 2) return false;
-  if (g_dbg & (1u << 21)) return true;  // diagnostics / tests: quad whenever it can launch
+  if (g_variant & FF_VARIANT_FORCE_QUAD) return true;  // A/B and tests: quad whenever it can launch
   // quads need an even ring count: when that costs a wave of units (OPT M=32768: 128 units
   // on 8 quad rings = 16 waves vs 9 pair rings = 15), plain pairs win (-2.4 %, A/B)
   const int waves_quad = (cfg->units + rings - 1) / rings, waves_pair = (cfg->units + pair_rings - 1) / pair_rings;
@@ -757,8 +825,7 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const int64_t max_rings =
       c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
   c->rings = (int32_t)std::min<int64_t>(units, max_rings);
-  plan_helpers(ch, c, num_sms);
-  c->grid_ctas = c->rings * c->ring * width + 2 * c->helpers;
+  c->grid_ctas = c->rings * c->ring * width;
   return FF_OK;
 }
 
@@ -791,9 +858,7 @@ const char* ff_last_error(void) { return g_last_error.c_str(); }
 // Diagnostics: when non-NULL, kernels write per-CTA wait-cycle counters
 // (unsigned long long[grid_ctas][16]) into this device buffer.
 void ff_set_profile_buffer(void* dev_ptr) { g_prof = reinterpret_cast<unsigned long long*>(dev_ptr); }
-// Diagnostics (not in the header's stable API): bit0 skip MMAs, bit1 skip ready-flag waits.
-// Results are wrong while set; used only by the feed-limit probes.
-void ff_set_debug_mode(int mode) { g_dbg = (uint32_t)mode; }
+void ff_set_variant(uint32_t flags) { g_variant = flags; }
 const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
 
 int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {
@@ -932,7 +997,7 @@ static int launch_common(const ffChainDesc* ch, const ffKernelConfig* cfg_in, co
   // L2 ready flags live in the lower half of the flag region (the pair
   // kernel's split slab flags use the upper half)
   if (cfg.exchange != FF_XCHG_DSM &&
-      (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kFlagBytes / 2)
+      (size_t)cfg.units * cfg.steps * cfg.ring * 2 * sizeof(uint32_t) > kRingFlagBytes)
     return fail(FF_ERR_UNSUPPORTED, "too many (unit, step, member) chunks for the flag region");
   if (cfg.n_splits > 1 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / cfg.lb) * sizeof(uint32_t) >= kCntBytes)
     return fail(FF_ERR_UNSUPPORTED, "too many E tiles for the split arrival counters");
@@ -959,9 +1024,11 @@ int ff_conv_chain_desc(const ffConvDesc* cv, ffChainDesc* out) {
   if (cv->k2 != 1 && cv->k1 != 1)
     return fail(FF_ERR_UNSUPPORTED, "one of the two convolutions must be pointwise (1x1)");
   if (cv->k1 % 2 == 0 || cv->k2 % 2 == 0) return fail(FF_ERR_UNSUPPORTED, "same padding needs an odd filter size");
-  if (cv->k2 > 1 && (cv->oc1 % 64 || cv->oc1 > 128 || (cv->oc2 != 64 && cv->oc2 != 128 && cv->oc2 != 256)))
-    return fail(FF_ERR_UNSUPPORTED,
-                "k2 x k2 second conv: oc1 in {64, 128} (whole intermediate per CTA), oc2 in {64, 128, 256}");
+  if (cv->k2 > 1 && cv->oc1 > 128)  // the whole 128-pixel intermediate tile stays in one CTA's TMEM / smem
+    return fail_capacity("C", "smem", (long long)(cv->oc1 - 128) * 128 * 2,
+                         "k2 x k2 second conv keeps every CTA's whole intermediate tile (oc1 <= 128 channels) on chip");
+  if (cv->k2 > 1 && (cv->oc1 % 64 || (cv->oc2 != 64 && cv->oc2 != 128 && cv->oc2 != 256)))
+    return fail(FF_ERR_UNSUPPORTED, "k2 x k2 second conv: oc1 in {64, 128}, oc2 in {64, 128, 256}");
   if (cv->k2 > 1 && (cv->k2 / 2 > 127 || cv->h > 65535 || cv->w > 65535))
     return fail(FF_ERR_UNSUPPORTED, "filter / feature map outside the im2col TMA ranges");
   if (cv->k1 > 1 && cv->ic % 64)
@@ -1036,10 +1103,27 @@ int ff_conv_chain_launch(const ffConvDesc* cv, const ffKernelConfig* cfg, const 
   return launch_common(&ch, cfg, t, ws, ws_bytes, nullptr, stream, cv);
 }
 
+// The plan's lowering under the first transport that executes it: CTA pairs
+// (cta_group::2, the production kernel), then the 1-CTA L2 and DSM kernels.
+static int lower_plan_any(const ffChainDesc* ch, const ffPlanDesc* plan, ffKernelConfig* cfg) {
+  int rc = FF_ERR_UNSUPPORTED;
+  for (int x : {FF_XCHG_L2_PAIR, FF_XCHG_L2, FF_XCHG_DSM}) {
+    rc = ff_plan_lower_ex(ch, plan, num_sms_cached(), x, cfg);
+    if (rc != FF_ERR_UNSUPPORTED) return rc;
+  }
+  return rc;
+}
+
+size_t ff_plan_workspace_bytes(const ffChainDesc* ch, const ffPlanDesc* plan) {
+  ffKernelConfig cfg;
+  if (lower_plan_any(ch, plan, &cfg)) return 0;
+  return ws_layout(ch, &cfg).total;
+}
+
 int ff_chain_run_plan(const ffChainDesc* ch, const ffPlanDesc* plan, const ffTensors* t, void* ws,
                       size_t ws_bytes, void* stream) {
   ffKernelConfig cfg;
-  int rc = ff_plan_lower(ch, plan, num_sms_cached(), &cfg);
+  int rc = lower_plan_any(ch, plan, &cfg);
   if (rc) return rc;
   return launch_common(ch, &cfg, t, ws, ws_bytes, nullptr, stream);
 }

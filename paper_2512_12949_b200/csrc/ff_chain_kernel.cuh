@@ -59,16 +59,12 @@ struct ChainArgs {
   int n_units;         // m_tiles * l_clusters * S
   int n_rings;         // rings launched (persistent)
   int act;
-  uint32_t epoch;      // unused (host-side epoch of earlier versions; see dev_epoch)
   uint32_t* dev_epoch; // workspace word: epoch of the last completed launch; this launch's flags use +1
   uint32_t* exit_cnt;  // workspace word (zero between launches): CTAs done; the last one advances dev_epoch
   __nv_bfloat16* E;    // output (S == 1)
   float* ws;           // fp32 accumulation workspace (S > 1)
   uint32_t* flags;     // L2 mode: [n_units][steps][G] chunk-ready flags
   float* slab;         // pair kernel: split-N exchange regions [E tile][split][16-B chunk][128 rows]
-  int helpers;         // pair kernel: helper pairs on the SMs the rings leave idle (0 = none)
-  int helper_x;        // pair kernel: last hops of every member's n-steps executed by the helpers
-  float* hzone;        // pair kernel: helper E partials, [E tile][n-step][16-B chunk][128 rows]
   uint32_t* tile_cnt;  // split-N arrival counters, one per 128-row E tile (zero between launches)
   __nv_bfloat16* c_debug;  // optional: dump of the bf16 intermediate (tests only)
   int defer;           // pair kernel: hops of step T that run after GEMM0(T+1) (< G)
@@ -76,6 +72,9 @@ struct ChainArgs {
   int krot;            // pair kernel: rotate each member's GEMM0 k order by its ring position
   int prefetch;        // pair kernel: L2 prefetch distance for weight tiles (k-blocks / hops), 0 = off
   int finish_tma;      // pair kernel: split finish by bulk copies (one unit per ring, 128/S % 8 == 0)
+  int c_slots;         // pair kernel: C exchange slots per ring member (scratch reused every c_slots n-steps)
+  int wpolicy;         // pair kernel: L2 hint (L2Hint) for weight tiles and their L2 prefetches
+  int cpolicy;         // pair kernel: L2 hint for the C exchange scratch (stores and loads)
   // conv chain as implicit GEMM (conv_k1 > 1): A is an NHWC feature map read
   // through an im2col tensor map; GEMM0 k-block kb = (filter tap, 64-channel block)
   int conv_k1;         // filter size of the first convolution (0: plain A[M][K])
@@ -87,7 +86,6 @@ struct ChainArgs {
   int conv2_k;
   int conv2_cblk;      // oc1 / 64
   int f16;             // 2-byte storage is fp16 (else bf16): MMA input format, C / E packing
-  uint32_t dbg;        // diagnostics only (ff_set_debug_mode): bit0 skip MMAs, bit1 skip ready-flag waits
   unsigned long long* prof;  // optional diagnostics: per CTA [FF_PROF_STRIDE] = 16 wait-cycle counters + 16 globaltimer stamps
 };
 
@@ -154,8 +152,12 @@ __device__ __forceinline__ void apply_act_frag(int act, float (&v)[N]) {
 // it, one idle thread counts the CTA in, and the last CTA to be counted (every
 // CTA has read by then) publishes this launch's epoch -- off the critical path.
 // Stream order keeps launches disjoint.
+// Flags are waited on for equality with the epoch (each flag slot is written
+// once per launch), so a slot last written any number of launches ago never
+// reads as current; 0 is skipped because it is the zero-filled initial state.
 __device__ __forceinline__ uint32_t epoch_begin(const ChainArgs& args) {
-  return ld_relaxed_gpu_u32(args.dev_epoch) + 1u;
+  const uint32_t e = ld_relaxed_gpu_u32(args.dev_epoch) + 1u;
+  return e != 0u ? e : 1u;
 }
 __device__ __forceinline__ void epoch_publish(const ChainArgs& args, uint32_t epoch) {
   if (atom_add_acqrel_gpu_u32(args.exit_cnt, 1u) == gridDim.x * gridDim.y * gridDim.z - 1u) {
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int tile = lo / C::BM; tile <= hi / C::BM; ++tile) {
             const uint32_t* f = args.flags + tile;  // unit id == m tile (ring 1, one step, one l cluster)
             uint32_t polls = 0;
-            FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - epoch) < 0) {
+            FF_TIMED(w_flag, while (ld_acquire_gpu_u32(f) != epoch) {
               if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
             });
           }
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(256, 1)
           // wait until ring member `origin` published chunk (unit, t)
           const uint32_t* f = flag_addr(u, t, origin);
           uint32_t polls = 0;
-          FF_TIMED(w_flag, while ((int)(ld_acquire_gpu_u32(f) - epoch) < 0) {
+          FF_TIMED(w_flag, while (ld_acquire_gpu_u32(f) != epoch) {
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
           });
           fence_proxy_async_global();
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(256, 1)
             uint32_t polls = 0;
             for (int j = 0; j < S; ++j) {
               if (j == sp) continue;
-              while ((int)(ld_relaxed_gpu_u32(flags + j) - epoch) < 0)
+              while (ld_relaxed_gpu_u32(flags + j) != epoch)
                 if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
             }
             fence_acq_rel_gpu();
@@ -829,7 +831,6 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
         for (int g0 = 0; g0 < kLB; g0 += cpt * tpr) {
           const int g1 = min(kLB, g0 + cpt * tpr);
-#pragma unroll 1
           // 16 columns of this thread's row into the SW128 staging tile
           auto stage16 = [&](int c0, const float* v) {
             const uint32_t rowb = stg + ((c0 - g0) / cpt) * 16384 + row * 128;

@@ -30,7 +30,8 @@ struct PairMaps {
   CUtensorMap b;    // std: B [K][N] 3D {64, K, N/64} box {64, 128, 2}; gated packed: [2][K][N] 4D box {64,128,1,2}
   CUtensorMap b1;   // gated, unpacked: B1 (3D, box {64, 128, 1}); b is then B0 with the same box
   CUtensorMap d;    // D [N][L]: 3D {64, N, L/64}, box {64, 128, 2}
-  CUtensorMap c;    // C scratch [Mpad][N]: 3D {64, Mpad, N/64}, box {64, 128, 2}
+  CUtensorMap c;    // C exchange scratch, box {64, 128, 2}: per-(ring, member, slot) regions of 256 rows x kN0
+                    // 3D {64, regions*256, kN0/64}; kRagged: the whole intermediate [Mpad][N], 3D {64, Mpad, N/64}
   CUtensorMap e;    // E [M][L] bf16: 2D box {64, 128}
   CUtensorMap w;    // fp32 workspace [M][L]: 2D box {32, 128}
   // single-instruction E tiles for a ring's final unit (stage area as staging):
@@ -94,24 +95,8 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t pq = kQuad ? crank >> 1 : 0u;  // pair within the quad (0 = X, 1 = Y)
   const uint32_t lrank = 2u * pq;        // this pair's leader rank in the cluster
   const bool leader = (q == 0);
-  // Helper pairs are spread over the grid (every `stride`-th pair) rather than
-  // appended: consecutive clusters fill a GPC, and 20 streaming helper SMs in
-  // one or two GPCs starve on the GPC's share of L2 bandwidth.  Virtual CTA
-  // index: members 0..member_ctas-1 in ring order, then the helpers.
-  const int member_ctas = args.n_rings * G * 2;
-  int vcta = (int)blockIdx.x;
-  if (!kQuad && args.helpers > 0) {
-    const int pi = (int)blockIdx.x / 2, H = args.helpers, stride = (member_ctas / 2 + H) / H;
-    if (pi % stride == stride - 1 && pi / stride < H)
-      vcta = member_ctas + 2 * (pi / stride) + (int)q;
-    else
-      vcta = 2 * (pi - min(H, (pi + 1) / stride)) + (int)q;
-  }
+  const int vcta = (int)blockIdx.x;
   if (threadIdx.x == 0) FF_STAMP(16);
-  if (args.dbg & (1u << 28)) {  // diagnostics: launch latency of this binary alone
-    if (threadIdx.x == 0) FF_STAMP(31);
-    return;
-  }
   const int p = kQuad ? (vcta / 4) % G : (vcta / 2) % G;  // ring position
   const int ring = kQuad ? 2 * ((vcta / 4) / G) + (int)pq : (vcta / 2) / G;
   const uint16_t mcast = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));  // this CTA and its twin
@@ -120,10 +105,7 @@ __global__ void __launch_bounds__(256, 1)
   // otherwise request the same A box at the same moment (one L2 slice set)
   const int krot = args.krot ? (p * kblocks / G) : 0;
   const int steps = args.steps;
-  const bool is_helper = vcta >= member_ctas;
-  const int hx = args.helpers > 0 ? args.helper_x : 0;     // hops per member n-step left to the helpers
-  const int my_units =
-      (!is_helper && ring < args.n_units) ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
+  const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
   const int total_steps = my_units * steps;
 
   struct Unit {
@@ -210,11 +192,26 @@ __global__ void __launch_bounds__(256, 1)
   // step 0, while the E accumulator is still unused, so it accumulates in E's TMEM
   // columns instead of waiting for the epilogue to drain C(0); E then lives in the
   // drained C columns.  Removes the C-drain bubble from the tensor pipe.
-  const bool swap_e = args.defer_last && total_steps == 2 && steps == 2 && hx == 0 && !(args.dbg & (1u << 30));
+  const bool swap_e = args.defer_last && total_steps == 2 && steps == 2;
   const uint32_t e_col = swap_e ? 0u : (uint32_t)C::kTMEM_E;
   auto c_col = [&](int T) { return (swap_e && T == 1) ? (uint32_t)C::kTMEM_E : 0u; };
   auto flag_addr = [&](const Unit& u, int t, int origin, int half) {
     return args.flags + (((size_t)u.id * steps + t) * G + origin) * 2 + half;
+  };
+  // C exchange scratch.  Chunk (global step T, origin) of this ring lives in region
+  // (ring, origin, T % c_slots); this CTA's half holds rows q*128.. of it.  A slot is
+  // rewritten c_slots steps later, once every member has read it: a member that has
+  // published its chunk of step T' has finished reading the chunks of step T'-2 (its
+  // GEMM0(T') MMAs, committed before the flag, were issued after its hops of T'-2, and
+  // tcgen05 MMAs complete in order), so before writing step T the origin waits for
+  // every member's flag of step T - c_slots + 2 (c_slots == 3; fewer slots only when a
+  // ring has no more steps than slots).  Ragged launches address the whole intermediate.
+  auto c_row = [&](const Unit& u, int T, int origin) {
+    if (kRagged) return u.m0 + (int)q * C::BM;
+    return ((ring * G + origin) * args.c_slots + T % args.c_slots) * (2 * C::BM) + (int)q * C::BM;
+  };
+  auto c_blk = [&](const Unit& u, int t, int origin) {  // first 64-column block of the chunk
+    return kRagged ? (u.n0 + (t * G + origin) * C::kN0) / 64 : 0;
   };
   const uint32_t L_c_empty = mapa(c_empty, lrank), L_own_full = mapa(own_full, lrank),
                  L_e_empty = mapa(e_empty, lrank);
@@ -226,210 +223,15 @@ __global__ void __launch_bounds__(256, 1)
   auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
   constexpr int kChunks = kLB / 4;  // 16-byte column chunks per E row
 
-  if (is_helper) {
-    // ===================== helper pair (SMs the rings leave idle) =====================
-    // A segment = (n-step t, m tile, member position p): the last hx hops of
-    // n-step t of member p in every N split's ring of that m tile (chunks of
-    // origins (p-h) mod G, h >= G-hx), which those members skip.  All of them
-    // accumulate into one TMEM E buffer (two buffers, alternating), drained by
-    // plain stores into the helper region (E tile, t); the members add the
-    // regions of every n-step, in order, in their split-N reduce-scatter
-    // (bit-reproducible: no atomics).
-    // Segments are listed position-major (p, m tile, then t); helper hp owns the
-    // contiguous block [hp*NS/H, (hp+1)*NS/H) and runs its step-0 segments first
-    // (their chunks are published first), then its step-1 segments.
-    const int H = args.helpers;
-    const int hp = (vcta - member_ctas) / 2;
-    const int NS = args.m_tiles * G * steps;
-    const int s_lo = (int)((long long)hp * NS / H), s_hi = (int)((long long)(hp + 1) * NS / H);
-    const int n_seg = s_hi - s_lo;
-    struct Seg {
-      int t, mt, p;
-    };
-    auto seg_of = [&](int i) {  // i-th segment in execution order
-      int sg = s_lo, t = 0;
-      for (t = 0; t < steps; ++t) {
-        const int first = s_lo + ((t - s_lo % steps) % steps + steps) % steps;  // first sg in range with sg%steps==t
-        const int cnt = first < s_hi ? (s_hi - 1 - first) / steps + 1 : 0;
-        if (i < cnt) {
-          sg = first + i * steps;
-          break;
-        }
-        i -= cnt;
-      }
-      const int mp = sg / steps;  // positions p-major: both m tiles of a p read the same D rows
-      return Seg{t, mp % args.m_tiles, mp / args.m_tiles};
-    };
-    auto unit_at = [&](const Seg& g, int split) {  // l_clusters == 1
-      return Unit{g.mt * 2 * C::BM, g.p * kLB, split * steps * G * C::kN0, g.mt + args.m_tiles * split, split};
-    };
-    // E buffer eb's barriers (selects, not a local array: a dynamically indexed
-    // array would give the kernel a stack frame)
-    auto hb_full = [&](int eb) { return eb ? c_full : e_full; };
-    auto hb_empty = [&](int eb) { return eb ? c_empty : e_empty; };
-    if (warp == 0) {
-      if (elect_one()) {
-        int stage = 0, phase = 0;
-        unsigned long long w_empty = 0, w_flag = 0;
-        const unsigned long long t_start = clock64();
-        const int nh = args.S * hx;  // hops per segment
-        auto hop_at = [&](const Seg& g, int hs, Unit& u, int& origin) {
-          u = unit_at(g, hs / hx);
-          origin = (g.p - (G - hx + hs % hx) + G) % G;
-        };
-        for (int i = 0; i < n_seg; ++i) {
-          const Seg g = seg_of(i);
-          const int dblk = g.p * kLB / 64 + (int)q * (kLB / 128);
-          // wait for every chunk of the segment at once: one round trip polls all
-          // missing flags (they are published together, at the end of GEMM0(t))
-          {
-            unsigned long long ready = 0ull;
-            const unsigned long long all = nh >= 64 ? ~0ull : (1ull << nh) - 1ull;
-            uint32_t polls = 0;
-            const unsigned long long tf0 = args.prof ? clock64() : 0ull;
-            while (ready != all) {
-              for (int h0 = 0; h0 < nh; h0 += 8) {
-                uint32_t v[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  v[j] = epoch;
-                  if (h0 + j < nh && !((ready >> (h0 + j)) & 1ull)) {
-                    Unit u;
-                    int origin;
-                    hop_at(g, h0 + j, u, origin);
-                    v[j] = ld_relaxed_gpu_u32(flag_addr(u, g.t, origin, (int)q));
-                  }
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (h0 + j < nh && (int)(v[j] - epoch) >= 0) ready |= 1ull << (h0 + j);
-              }
-              if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
-            }
-            if (args.prof) w_flag += clock64() - tf0;
-            fence_acq_rel_gpu();
-            fence_proxy_async_global();
-          }
-          for (int hs = 0; hs < nh; ++hs) {
-            Unit u;
-            int origin;
-            hop_at(g, hs, u, origin);
-            const int ncol0 = u.n0 + (g.t * G + origin) * C::kN0;
-            if (hs + 2 < nh) {  // D rows two hops ahead into L2 (weights stream from HBM)
-              Unit u2;
-              int o2;
-              hop_at(g, hs + 2, u2, o2);
-              const int nc2 = u2.n0 + (g.t * G + o2) * C::kN0;
-              for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) tma_prefetch_l2_3d(&maps.d, 0, nc2 + kb2 * C::BK, dblk);
-            }
-            for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-              FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
-              const uint32_t sb = base + stage * C::kSTAGE;
-              const uint32_t lb = mapa(full_bar(stage), lrank);
-              if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
-              tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
-              tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
-              if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1;
-              }
-            }
-          }
-        }
-        if (args.prof) {
-          unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
-          pr[0] = clock64() - t_start;
-          pr[1] = w_empty;
-          pr[2] = w_flag;
-        }
-      }
-    } else if (warp == 1) {
-      if (leader && elect_one()) {
-        const uint32_t idesc1 = idesc_as(idesc_bf16(256, kLB, 0, 1), args.f16);
-        int stage = 0, phase = 0;
-        unsigned long long w_full = 0, w_buf = 0;
-        const unsigned long long t_start = clock64();
-        for (int i = 0; i < n_seg; ++i) {
-          const int eb = i & 1;
-          if (i >= 2) {
-            FF_TIMED(w_buf, mbar_wait_cluster(hb_empty(eb), ((i >> 1) - 1) & 1));
-            tc_fence_after();
-          }
-          bool started = false;
-          for (int hs = 0; hs < args.S * hx; ++hs) {
-            for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
-              FF_TIMED(w_full, mbar_wait(full_bar(stage), phase));
-              tc_fence_after();
-              const uint32_t sb = base + stage * C::kSTAGE;
-#pragma unroll
-              for (int kk = 0; kk < C::BK / 16; ++kk) {
-                umma_bf16_pair(tmem_base + eb * C::kTMEM_E, a_desc(sb, kk), b_desc(sb + C::kSLOT, kk), idesc1,
-                               started ? 1u : 0u);
-                started = true;
-              }
-              umma_commit_pair(empty_bar(stage), kPairMask);
-              if (++stage == kStages) {
-                stage = 0;
-                phase ^= 1;
-              }
-            }
-          }
-          umma_commit_pair(hb_full(eb), kPairMask);
-        }
-        if (args.prof) {
-          unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
-          pr[3] = clock64() - t_start;
-          pr[4] = w_full;
-          pr[8] = w_buf;
-        }
-      }
-    } else if (warp >= 4) {
-      const int wq = warp & 3;
-      const int row = wq * 32 + (int)lane_id();
-      const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
-      for (int i = 0; i < n_seg; ++i) {
-        const int eb = i & 1;
-        mbar_wait_cluster(hb_full(eb), (i >> 1) & 1);
-        tc_fence_after();
-        if (warp == 4 && lane_id() == 0 && i < 6) FF_STAMP(18 + i);  // diagnostics: segment i's MMAs done
-        const Seg g = seg_of(i);
-        const int erow = g.mt * 2 * C::BM + (int)q * C::BM;
-        const int tile = (erow / C::BM) * (args.L / kLB) + g.p;
-        // plain coalesced stores into the segment's own region (tile, t): a warp's
-        // 32 rows of one 16-byte column chunk are 512 contiguous bytes
-        float* const dst = args.hzone + ((size_t)tile * steps + g.t) * (kChunks * 128 * 4) + row * 4;
-        const int c_end = (args.dbg & (1u << 25)) ? 0 : kLB;  // diagnostics: skip the drain
-#pragma unroll 1
-        for (int c0 = 0; c0 < c_end; c0 += 64) {
-          float v[32], w[32];
-          tmem_ld32x2(lane_base + eb * C::kTMEM_E + c0, lane_base + eb * C::kTMEM_E + c0 + 32, v, w);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            st_global_v4(dst + (size_t)(c0 / 4 + j) * 512, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
-                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
-            st_global_v4(dst + (size_t)(c0 / 4 + 8 + j) * 512, __float_as_uint(w[4 * j]), __float_as_uint(w[4 * j + 1]),
-                         __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
-          }
-        }
-        // TMEM buffer free: tcgen05 loads waited + fenced; the arrive publishes no data
-        tc_fence_before();
-        mbar_arrive_remote_relaxed(mapa(hb_empty(eb), lrank));
-        // region complete: the barrier orders the 128 threads' stores before the
-        // issuer's gpu-scope release (cumulative), no per-thread fence
-        named_bar_sync(1, 128);
-        if (warp == 4 && lane_id() == 0) {
-          red_add_release_gpu_u32(args.tile_cnt + tile, 1u);
-          if (i < 6) FF_STAMP(24 + i);  // diagnostics: segment i drained
-        }
-      }
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (elect_one()) {
       unsigned long long w_empty = 0, w_flag = 0;
       const unsigned long long t_start = clock64();
       int stage = 0, phase = 0;
-      uint32_t seq = 0;  // stage-load sequence number (identical in both pairs of a quad)
+      uint32_t seq = 0;
+      const uint64_t pol_w = l2_policy(args.wpolicy);  // weight tiles (B / gate|up, D)
+      const uint64_t pol_c = l2_policy(args.cpolicy);  // C exchange scratch  // stage-load sequence number (identical in both pairs of a quad)
       auto next = [&]() {
         if (++stage == kStages) {
           stage = 0;
@@ -463,27 +265,27 @@ __global__ void __launch_bounds__(256, 1)
           if (pf && kbl + pf < kblocks && (!kQuad || pq == 0)) {
             const int kbp = (kbl + pf + krot) % kblocks;
             if (!kGated || !kPackedB)
-              tma_prefetch_l2_3d(&maps.b, 0, kbp * C::BK, nblk);
+              tma_prefetch_l2_3d_h(&maps.b, 0, kbp * C::BK, nblk, pol_w);
             else
-              tma_prefetch_l2_4d(&maps.b, 0, kbp * C::BK, nblk, 0);
+              tma_prefetch_l2_4d_h(&maps.b, 0, kbp * C::BK, nblk, 0, pol_w);
           }
           if (!mine) {
           } else if (kQuad) {
             if (!kGated) {
-              tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast);
+              tma_load_3d_pair_mcast_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast, pol_w);
             } else if (kPackedB) {
-              tma_load_4d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0, mcast);
+              tma_load_4d_pair_mcast_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0, mcast, pol_w);
             } else {
-              tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast);
-              tma_load_3d_pair_mcast(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk, mcast);
+              tma_load_3d_pair_mcast_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, mcast, pol_w);
+              tma_load_3d_pair_mcast_h(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk, mcast, pol_w);
             }
           } else if (!kGated) {
-            tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
+            tma_load_3d_pair_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, pol_w);
           } else if (kPackedB) {
-            tma_load_4d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0);
+            tma_load_4d_pair_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, 0, pol_w);
           } else {
-            tma_load_3d_pair(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk);
-            tma_load_3d_pair(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk);
+            tma_load_3d_pair_h(sb + C::kSLOT, &maps.b, lb, 0, kb * C::BK, nblk, pol_w);
+            tma_load_3d_pair_h(sb + C::kSLOT + C::kSLOT / 2, &maps.b1, lb, 0, kb * C::BK, nblk, pol_w);
           }
           next();
         }
@@ -498,7 +300,7 @@ __global__ void __launch_bounds__(256, 1)
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
         if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
         if (!has_chunk(T, origin)) return;  // ragged n-step: no chunk from this origin
-        if (from_l2 && !((ready >> origin) & 1ull) && !(args.dbg & 2u)) {
+        if (from_l2 && !((ready >> origin) & 1ull)) {
           // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
           FF_TIMED(w_flag, do {
@@ -511,7 +313,7 @@ __global__ void __launch_bounds__(256, 1)
                            : epoch - 1u;
 #pragma unroll
               for (int j = 0; j < 8; ++j)
-                if ((int)(v[j] - epoch) >= 0) ready |= 1ull << (o0 + j);
+                if (v[j] == epoch) ready |= 1ull << (o0 + j);
             }
             if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
           } while (!((ready >> origin) & 1ull)));
@@ -520,18 +322,20 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
           const int ncol_pf = u.n0 + (t * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
-          for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) tma_prefetch_l2_3d(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk);
+          for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
+            tma_prefetch_l2_3d_h(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk, pol_w);
         }
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
           if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
-          if (from_l2) tma_load_3d_pair(sb, &maps.c, lb, 0, u.m0 + (int)q * C::BM, (ncol0 + kb2 * C::BK) / 64);
+          if (from_l2)
+            tma_load_3d_pair_h(sb, &maps.c, lb, 0, c_row(u, T, origin), c_blk(u, t, origin) + kb2 * (C::BK / 64), pol_c);
           if (!kQuad)
-            tma_load_3d_pair(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk);
+            tma_load_3d_pair_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, pol_w);
           else if ((seq++ & 1u) == pq)
-            tma_load_3d_pair_mcast(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, mcast);
+            tma_load_3d_pair_mcast_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, mcast, pol_w);
           next();
         }
       };
@@ -539,7 +343,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
           if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          if (h < G - hx) load_hop(T, h);  // the last hx hops run on the helpers
+          load_hop(T, h);
         }
       }
       if (args.prof) {
@@ -579,7 +383,6 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             const uint64_t ad = a_desc(sb, kk);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (args.dbg & 1u) continue;
             if (kGated) {
               umma_bf16_pair(cacc, ad, b_desc(sb + C::kSLOT, kk), idesc0, acc);
               umma_bf16_pair(cacc + C::kN0, ad, b_desc(sb + C::kSLOT + C::kSLOT / 2, kk), idesc0, acc);
@@ -616,8 +419,7 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t aslot = (C::kOwnFull && h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
-            if (!(args.dbg & 1u))
-              umma_bf16_pair(tmem_base + e_col, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
+            umma_bf16_pair(tmem_base + e_col, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
                              e_started ? 1u : 0u);
             e_started = true;
           }
@@ -625,13 +427,13 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
         if (C::kOwnFull && h == 0) umma_commit_pair(own_free, kPairMask);
-        if (t == steps - 1 && h == G - 1 - hx) umma_commit_pair(e_full, kPairMask);
+        if (t == steps - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
       };
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         for (int h = 0; h < G; ++h) {
           if (T + 1 < total_steps) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          if (h < G - hx) hop(T, h);
+          hop(T, h);
         }
       }
       if (args.prof) {
@@ -654,6 +456,33 @@ __global__ void __launch_bounds__(256, 1)
     const unsigned long long t_start = clock64();
     // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
     auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
+    const uint64_t pol_c = l2_policy(args.cpolicy);  // C exchange scratch
+    // before chunk T overwrites slot T % c_slots: every ring member's flag of step
+    // T - c_slots + 2, i.e. all of them have read step T - c_slots (see c_row)
+    auto wait_slot_free = [&](int T) {
+      if (kRagged || T < args.c_slots) return;
+      const int Tp = T - args.c_slots + 2;
+      const Unit up = unit_of(Tp / steps);
+      const int tp = Tp % steps;
+      uint32_t polls = 0;
+      unsigned long long seen = 0ull;
+      const unsigned long long all = G >= 64 ? ~0ull : (1ull << G) - 1ull;
+      while (seen != all) {
+        for (int o0 = 0; o0 < G; o0 += 8) {
+          uint32_t v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)  // independent loads: in flight together
+            v[j] = (o0 + j < G && !((seen >> (o0 + j)) & 1ull)) ? ld_relaxed_gpu_u32(flag_addr(up, tp, o0 + j, (int)q))
+                                                                 : epoch;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (o0 + j < G && v[j] == epoch) seen |= 1ull << (o0 + j);
+        }
+        if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+      }
+      fence_acq_rel_gpu();
+      fence_proxy_async_global();
+    };
     // C chunk of global step T: TMEM -> activation / gate -> bf16 SW128 own slot -> L2 scratch + flag
     auto drain_c = [&](int T) {
       const Unit u = unit_of(T / steps);
@@ -664,7 +493,6 @@ __global__ void __launch_bounds__(256, 1)
       FF_TIMED(w_ofree, mbar_wait_cluster(own_free, (T & 1) ^ 1));
       const unsigned long long t_d0 = args.prof ? clock64() : 0ull;
       const bool publish = G > 1 || !C::kOwnFull;  // the chunk goes to the L2 scratch
-      const int nblk = (u.n0 + (t * G + p) * C::kN0) / 64;
       constexpr int kRoundCols = C::kOWN_BYTES / (C::BM * 2);  // 128 columns per own-slot round
       const bool has = has_chunk(T, p);
       if (!has) {  // ragged last n-step without a chunk here: the handshakes only
@@ -715,7 +543,8 @@ __global__ void __launch_bounds__(256, 1)
         if (publish) {
           named_bar_sync(1, 128);
           if (issuer) {
-            tma_store_3d(&maps.c, own_slot, 0, u.m0 + (int)q * C::BM, nblk + r0 / 64);
+            if (r0 == 0) wait_slot_free(T);
+            tma_store_3d_h(&maps.c, own_slot, 0, c_row(u, T, p), c_blk(u, t, p) + r0 / 64, pol_c);
             bulk_commit();
           }
         }
@@ -747,7 +576,7 @@ __global__ void __launch_bounds__(256, 1)
         // drain and publish it before this unit's E, so the tensor core can start the
         // next GEMM0 while E drains (not with kOwnFull: the own slot then still holds
         // that chunk as hop 0's operand when E needs it for staging).
-        if (!C::kOwnFull && T + 1 < total_steps && !(args.dbg & (1u << 31))) {
+        if (!C::kOwnFull && T + 1 < total_steps) {
           drain_c(T + 1);
           next_c = T + 2;
         }
@@ -798,10 +627,6 @@ __global__ void __launch_bounds__(256, 1)
           if (issuer) {
             if (bf16_out)
               tma_store_3d(&maps.e3, base, 0, erow, u.l0 / 64);
-            else if (args.dbg & 8u)  // diagnostics: plain store instead of reduce-add (wrong sums)
-              tma_store_3d(&maps.w3, base, 0, erow, u.l0 / 32);
-            else if (args.dbg & 16u)  // diagnostics: eight 16 KB reduce-adds instead of one 128 KB
-              for (int c = 0; c < kLB / 32; ++c) tma_reduce_add_2d(&maps.w, base + c * 16384, u.l0 + 32 * c, erow);
             else
               tma_reduce_add_3d(&maps.w3, base, 0, erow, u.l0 / 32);
             bulk_commit();
@@ -947,12 +772,9 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t polls = 0;
       for (int j = 0; j < S; ++j) {
         if (j == sp) continue;
-        while ((int)(ld_relaxed_gpu_u32(slab_flag(j)) - epoch) < 0)
+        while (ld_relaxed_gpu_u32(slab_flag(j)) != epoch)
           if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
       }
-      if (hx > 0)  // every helper segment (one per n-step) of this tile is in its region
-        while ((int)(ld_relaxed_gpu_u32(args.tile_cnt + tile) - (uint32_t)steps) < 0)
-          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
       fence_acq_rel_gpu();
       fence_proxy_async_global();
       if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 27] = globaltimer_ns();
@@ -965,16 +787,13 @@ __global__ void __launch_bounds__(256, 1)
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
     // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
     const uint8_t* const src = smem_gen;
-    const int n_items = (args.dbg & 32u) ? 0 : R * kChunks;  // diagnostics: skip the sum
+    const int n_items = R * kChunks;
     // R = 128 / S is a power of two (pair_finish_regions): item -> (chunk, row) by shifts (a
     // runtime division per item made the sum ~3x slower than its shared-memory traffic).
     // A thread takes the two fp32 column chunks 2cp, 2cp+1 of one row: their bf16 result is
     // one 16-byte SW128 chunk, so 8 consecutive rows fill all 32 banks (one wavefront).
     const int rs = 31 - __clz(R);
     const int n_pairs = n_items / 2;
-    // helper regions (tile, t) of this slice's rows: coalesced global loads (item -> 16 B,
-    // consecutive threads -> consecutive rows of one column chunk)
-    const float* const hreg = args.hzone + (size_t)tile * steps * (kChunks * 128 * 4) + sp * R * 4;
 #pragma unroll 1
     for (int p0 = tid; p0 < n_pairs; p0 += 512) {
 #pragma unroll
@@ -992,14 +811,6 @@ __global__ void __launch_bounds__(256, 1)
           a0.x += f0.x; a0.y += f0.y; a0.z += f0.z; a0.w += f0.w;
           a1.x += f1.x; a1.y += f1.y; a1.z += f1.z; a1.w += f1.w;
         }
-        if (hx > 0) {  // then the helpers' n-step partials, in order
-          for (int t2 = 0; t2 < steps && t2 < 2; ++t2) {
-            const float* h = hreg + (size_t)t2 * (kChunks * 128 * 4) + rr * 4;
-            const float4 g0 = ld_global_f4(h + (size_t)(2 * cp) * 512), g1 = ld_global_f4(h + (size_t)(2 * cp + 1) * 512);
-            a0.x += g0.x; a0.y += g0.y; a0.z += g0.z; a0.w += g0.w;
-            a1.x += g1.x; a1.y += g1.y; a1.z += g1.z; a1.w += g1.w;
-          }
-        }
         st_shared_v4(ebuf + (cp / 8) * (R * 128) + rr * 128 + (((cp % 8) ^ (rr & 7)) << 4),
                      pack2(args.f16, a0.x, a0.y), pack2(args.f16, a0.z, a0.w), pack2(args.f16, a1.x, a1.y),
                      pack2(args.f16, a1.z, a1.w));
@@ -1012,8 +823,6 @@ __global__ void __launch_bounds__(256, 1)
       tma_store_3d(&maps.er, ebuf, 0, erow + sp * R, u.l0 / 64);
       bulk_commit();
       FF_STAMP(26);
-      if (hx > 0 && atom_add_acqrel_gpu_u32(args.tile_cnt + tile, 1u) == (uint32_t)(steps + S - 1))
-        *reinterpret_cast<volatile uint32_t*>(args.tile_cnt + tile) = 0u;  // all splits past their wait
       bulk_wait_read0();
     }
   }

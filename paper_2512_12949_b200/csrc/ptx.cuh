@@ -345,6 +345,73 @@ __device__ __forceinline__ void tma_store_2d(const void* desc, uint32_t src, int
                "r"(src), "r"(c0), "r"(c1)
                : "memory");
 }
+// ---- L2 cache policies (createpolicy) and hinted TMA forms ----
+// Weights streamed once get evict_first, the C exchange scratch evict_last (it
+// must stay on chip until every ring member has read it); 0 = no hint.
+enum L2Hint : int { L2_NORMAL = 0, L2_EVICT_FIRST = 1, L2_EVICT_LAST = 2 };
+__device__ __forceinline__ uint64_t l2_policy(int hint) {
+  uint64_t p;
+  if (hint == L2_EVICT_FIRST)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (hint == L2_EVICT_LAST)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_pair_h(uint32_t dst, const void* desc, uint32_t leader_bar, int32_t c0,
+                                                   int32_t c1, int32_t c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_h(uint32_t dst, const void* desc, uint32_t leader_bar, int32_t c0,
+                                                   int32_t c1, int32_t c2, int32_t c3, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair_mcast_h(uint32_t dst, const void* desc, uint32_t leader_bar,
+                                                         int32_t c0, int32_t c1, int32_t c2, uint16_t mask,
+                                                         uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "h"(mask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_mcast_h(uint32_t dst, const void* desc, uint32_t leader_bar,
+                                                         int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                                                         uint16_t mask, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7, %8;" ::"r"(dst),
+      "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar), "h"(mask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d_h(const void* desc, uint32_t src, int32_t c0, int32_t c1, int32_t c2,
+                                               uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+                   desc),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_3d_h(const void* desc, int32_t c0, int32_t c1, int32_t c2,
+                                                     uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.L2::cache_hint [%0, {%1, %2, %3}], %4;" ::"l"(desc),
+               "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_4d_h(const void* desc, int32_t c0, int32_t c1, int32_t c2,
+                                                     int32_t c3, uint64_t pol) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.L2::cache_hint [%0, {%1, %2, %3, %4}], %5;" ::"l"(desc),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+               : "memory");
+}
 // Bulk-group completion (TMA stores / bulk_group copies only -- NOT the
 // mbarrier-completed shared::cluster copies).
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }

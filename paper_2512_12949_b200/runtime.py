@@ -113,31 +113,61 @@ def _workspace(nbytes: int, device, stream):
     return buf
 
 
+def _check_out(out, shape, like):
+    """A caller-supplied output must be a contiguous CUDA tensor of the inputs'
+    dtype, exact shape and device: the kernel writes it through a TMA map built
+    from the shape with a dense row stride (and plain stores in the split finish)."""
+    if (not out.is_cuda or out.device != like.device or out.dtype != like.dtype or tuple(out.shape) != tuple(shape)
+            or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous {like.dtype} CUDA tensor of shape {tuple(shape)} on {like.device}")
+    if out.data_ptr() % 16:
+        raise ValueError("out must be 16-byte aligned")
+
+
+def _stream_of(stream, device):
+    """torch stream for `stream` (None = current stream, or a raw cudaStream_t handle)."""
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    if not hasattr(s, "cuda_stream"):
+        s = torch.cuda.ExternalStream(int(s), device=device)
+    return s
+
+
+def _require_cuda():
+    import torch
+
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
+        globals()["_cuda_ok"] = True
+
+
 def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, stream=None, c_debug=None):
     """Launch one fused chain with an explicit physical configuration."""
     import torch
 
     lib = nat.load()
-    if not _cuda_ok:
-        if not torch.cuda.is_available():
-            raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
-        globals()["_cuda_ok"] = True
+    _require_cuda()
     gated = graph.kind == GATED_FFN
     names = ("A", "B0", "B1", "D") if gated else ("A", "B", "D")
     d = graph.dims
     shapes = {"A": (d.m, d.k), "B": (d.k, d.n), "B0": (d.k, d.n), "B1": (d.k, d.n), "D": (d.n, d.l)}
     storage = _storage([tensors[n] for n in names])
+    a = tensors["A"]
     for name in names:
         t = tensors[name]
-        if not t.is_cuda or tuple(t.shape) != shapes[name] or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]}")
+        if (not t.is_cuda or t.device != a.device or tuple(t.shape) != shapes[name] or not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]} on "
+                             f"{a.device}")
         if t.data_ptr() % 16:
             raise ValueError(f"{name} must be 16-byte aligned")
-    a = tensors["A"]
     if out is None:
         out = torch.empty((d.m, d.l), dtype=a.dtype, device=a.device)
-    elif out.dtype != a.dtype:
-        raise ValueError("out must have the inputs' dtype")
+    else:
+        _check_out(out, (d.m, d.l), a)
+    if c_debug is not None:
+        _check_out(c_debug, (d.m, d.n), a)
     # descriptor + workspace size per (chain, storage, launch config): a serving loop
     # calls this with the same shapes every step (host cost ~15 -> ~8 us per launch)
     key = (graph.kind, graph.activation, d.m, d.n, d.k, d.l, storage, bytes(cfg))
@@ -149,9 +179,7 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
             _desc_cache.clear()
         _desc_cache[key] = cached
     ch, ws_bytes = cached
-    s = stream if stream is not None else torch.cuda.current_stream(a.device)
-    if not hasattr(s, "cuda_stream"):
-        s = torch.cuda.ExternalStream(int(s), device=a.device)
+    s = _stream_of(stream, a.device)
     handle = s.cuda_stream
     ws = _workspace(ws_bytes, a.device, s)
     tp = nat.Tensors(a.data_ptr(), tensors["B0" if gated else "B"].data_ptr(),
@@ -197,7 +225,7 @@ def profile_best_from_list(graph: ChainGraph, plans, tensors: dict, iters: int =
         if key in seen:
             continue
         seen.add(key)
-        out = torch.empty((graph.dims.m, graph.dims.l), dtype=torch.bfloat16, device="cuda")
+        out = torch.empty((graph.dims.m, graph.dims.l), dtype=tensors["A"].dtype, device=tensors["A"].device)
         for _ in range(warmup):
             launch(graph, cfg, tensors, out=out)
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -216,7 +244,7 @@ def profile_configs(graph: ChainGraph, cfgs, tensors: dict, iters: int = 10, war
     import torch
 
     out = []
-    res = torch.empty((graph.dims.m, graph.dims.l), dtype=torch.bfloat16, device="cuda")
+    res = torch.empty((graph.dims.m, graph.dims.l), dtype=tensors["A"].dtype, device=tensors["A"].device)
     for cfg in cfgs:
         for _ in range(warmup):
             launch(graph, cfg, tensors, out=res)
@@ -266,20 +294,24 @@ def launch_conv(cfg, kcfg: nat.KernelConfig, x, w1, w2, out=None, stream=None, a
     import torch
 
     lib = nat.load()
-    if not torch.cuda.is_available():
-        raise nat.NativeUnavailable("no CUDA device: the fused chain only executes on sm_100a")
+    _require_cuda()
     batch = x.shape[0]
     w2_shape = (cfg.oc1, cfg.oc2) if cfg.k2 == 1 else (cfg.k2, cfg.k2, cfg.oc1, cfg.oc2)
     shapes = {"x": (batch, cfg.h, cfg.w, cfg.ic), "w1": (cfg.k1, cfg.k1, cfg.ic, cfg.oc1), "w2": w2_shape}
     storage = _storage([x, w1, w2])
     for name, t in (("x", x), ("w1", w1), ("w2", w2)):
-        if not t.is_cuda or tuple(t.shape) != shapes[name] or not t.is_contiguous():
-            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]}")
+        if not t.is_cuda or t.device != x.device or tuple(t.shape) != shapes[name] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous {storage} CUDA tensor of shape {shapes[name]} on "
+                             f"{x.device}")
+        if t.data_ptr() % 16:
+            raise ValueError(f"{name} must be 16-byte aligned")
     if out is None:
         out = torch.empty((batch, cfg.h, cfg.w, cfg.oc2), dtype=x.dtype, device=x.device)
+    else:
+        _check_out(out, (batch, cfg.h, cfg.w, cfg.oc2), x)
     cd = conv_desc(cfg, batch, activation, storage)
     ws_bytes = lib.ff_conv_chain_workspace_bytes(ctypes.byref(cd), ctypes.byref(kcfg))
-    s = stream if stream is not None else torch.cuda.current_stream(x.device)
+    s = _stream_of(stream, x.device)
     ws = _workspace(ws_bytes, x.device, s)
     tp = nat.Tensors(x.data_ptr(), w1.data_ptr(), None, w2.data_ptr(), out.data_ptr())
     nat.check(lib.ff_conv_chain_launch(ctypes.byref(cd), ctypes.byref(kcfg), ctypes.byref(tp),

@@ -72,6 +72,10 @@ def run_sharded(graph: ChainGraph, tensors: dict, group=None, gather: bool = Fal
     if not gather or world == 1:
         return out
     sizes = [shard_bounds(graph.dims.m, world, r) for r in range(world)]
-    parts = [torch.empty((h - l_, graph.dims.l), dtype=out.dtype, device=out.device) for l_, h in sizes]
-    dist.all_gather(parts, out.contiguous(), group=group)
-    return torch.cat(parts)
+    # NCCL gathers device tensors over NVLink; gloo (CPU process groups, ranks sharing
+    # a GPU in tests) gathers host copies
+    on_host = dist.get_backend(group) == "gloo"
+    dev = torch.device("cpu") if on_host else out.device
+    parts = [torch.empty((h - l_, graph.dims.l), dtype=out.dtype, device=dev) for l_, h in sizes]
+    dist.all_gather(parts, out.contiguous().to(dev), group=group)
+    return torch.cat(parts).to(out.device)

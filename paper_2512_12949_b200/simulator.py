@@ -347,6 +347,13 @@ def verify(plan: FusionPlan, graph: ChainGraph, config: SimConfig = SimConfig(),
 def unfused_baseline(graph: ChainGraph, inputs: dict, plan: FusionPlan):
     """Byte model of the two-kernel path, intermediate round-tripping global
     memory (simulator.py:495-556); E computed by two cuBLAS GEMMs + act."""
+    trace = unfused_traffic(graph, plan)
+    return oracle(graph, {k: _to_device(v) for k, v in inputs.items()}), trace
+
+
+def unfused_traffic(graph: ChainGraph, plan: FusionPlan) -> TrafficTrace:
+    """The byte trace of unfused_baseline alone (no inputs, no execution):
+    tile loads replayed with singleton clusters, C stored in full and read once."""
     d = graph.dims
     elt = d.element_size
     blk = plan.tiles.block
@@ -379,7 +386,7 @@ def unfused_baseline(graph: ChainGraph, inputs: dict, plan: FusionPlan):
     trace.add_load("C", c_bytes)
     kernel_loads(("m", "n", "l"), [("D", ("n", "l"), blk["n"] * blk["l"] * elt)])
     trace.add_store("E", d.m * d.l * elt * ((d.n // blk["n"]) if "n" in sched.spatial else 1))
-    return oracle(graph, {k: _to_device(v) for k, v in inputs.items()}), trace
+    return trace
 
 
 def sample_valid_plans(graph: ChainGraph, device: DeviceModel, count: int, seed: int = 0,

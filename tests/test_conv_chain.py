@@ -70,8 +70,11 @@ def test_block_config_rules():
     for exchange in ("dsm", "pair"):
         with pytest.raises(nat.UnsupportedPlan):
             runtime.lower_conv(W.ConvBlockConfig(256, 56, 56, 64, 64, 1, 3), exchange=exchange)
-    with pytest.raises(nat.UnsupportedPlan):  # the whole intermediate of a tile: oc1 <= 128
+    from paper_2512_12949_b200.errors import CapacityExceeded
+
+    with pytest.raises(CapacityExceeded) as info:  # the whole intermediate of a tile: oc1 <= 128
         runtime.lower_conv(W.ConvBlockConfig(256, 14, 14, 256, 64, 1, 3), exchange="l2")
+    assert (info.value.tensor, info.value.floor, info.value.unplaced) == ("C", "smem", 128 * 128 * 2)
 
 
 @pytest.mark.parametrize("k1", [1, 3, 5])

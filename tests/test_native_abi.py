@@ -178,3 +178,18 @@ def test_launch_argument_errors_without_touching_the_gpu(lib):
     bad_dtype = runtime.chain_desc(graph)
     bad_dtype.dtype = 7
     assert lib.ff_chain_launch(ctypes.byref(bad_dtype), ctypes.byref(cfg), ctypes.byref(ok), 0x100000, need, None) == 5
+
+
+def test_run_plan_rejects_plans_without_lowering(lib):
+    """ff_chain_run_plan / ff_plan_workspace_bytes on a plan the lowering refuses: a
+    status code and a message, workspace size 0, nothing launched (no GPU needed)."""
+    graph = W.build_standard_ffn(W.DimensionSpec(256, 1024, 256, 1024), "relu")
+    plan = make_plan("n", "klm", (64, 256, 512, 256), (1, 4, 1, 4), "doubled_k")  # gated lowering, standard chain
+    ch, pd = runtime.chain_desc(graph), runtime.plan_desc(plan)
+    assert lib.ff_plan_workspace_bytes(ctypes.byref(ch), ctypes.byref(pd)) == 0
+    t = nat.Tensors(256, 256, None, 256, 256)
+    rc = lib.ff_chain_run_plan(ctypes.byref(ch), ctypes.byref(pd), ctypes.byref(t), None, 0, None)
+    assert rc == nat.FF_ERR_PLAN
+    assert b"gated lowering" in lib.ff_last_error()
+    with pytest.raises(PlanError):
+        nat.check(rc)

@@ -1,0 +1,103 @@
+"""Per-CTA phase timeline of a fused-chain launch (diagnostics, GPU box only).
+
+    python tools/timeline.py [gpt67b|llama|opt|gpt2s ...] [x0|x1] [warm] [rings] [variant=0x..]
+
+Every CTA stamps %globaltimer at fixed points (slots 16..31 of the profile
+buffer, ff_set_profile_buffer); this prints min / mean / max per stamp relative
+to the first CTA's entry, for the median of 5 launches on a cold L2 (flushed
+before each launch, as bench.py does).  x0 / x1 select the 1-CTA DSM / L2
+kernels (default: the CTA-pair kernel)."""
+
+import ctypes
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_12949_b200 import _native as nat  # noqa: E402
+
+ST = 32
+NAMES = {0: 'entry', 1: 'setup', 2: 'cfull0', 3: 'drained0', 4: 'stored0', 5: 'cfull1', 6: 'E_summed',
+         7: 'drained1', 8: 'E_staged', 9: 'E_slabs_out', 10: 'E_finished', 11: 'E_flags_in', 12: 'E_loaded',
+         13: 'E_sum0', 14: 'E_start', 15: 'exit'}
+SHAPES = {"llama": (512, 8192, 2048, 2048, 2, True), "gpt67b": (512, 16384, 4096, 4096, 1, False),
+          "opt": (4096, 8192, 2048, 2048, 1, False), "gpt2s": (512, 3072, 768, 768, 3, False)}
+
+
+def setup(m, n, k, l, act, gated, xchg, lib):
+    a = (torch.rand(m, k, device='cuda') * 2 - 1).bfloat16()
+    if gated:
+        b01 = (torch.rand(2, k, n, device='cuda') * 2 - 1).bfloat16()
+        b, b1 = b01[0], b01[1]
+    else:
+        b = (torch.rand(k, n, device='cuda') * 2 - 1).bfloat16()
+        b1 = b
+    d = (torch.rand(n, l, device='cuda') * 2 - 1).bfloat16()
+    e = torch.zeros(m, l, device='cuda', dtype=torch.bfloat16)
+    ch = nat.ChainDesc(1 if gated else 0, 2 if gated else act, m, n, k, l, 2, 0)
+    kc = nat.KernelConfig()
+    nat.check(lib.ff_auto_config_ex(ctypes.byref(ch), 148, xchg, ctypes.byref(kc)))
+    ws = torch.zeros(lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(kc)) or 256, device='cuda',
+                     dtype=torch.uint8)
+    t = nat.Tensors(a.data_ptr(), b.data_ptr(), b1.data_ptr(), d.data_ptr(), e.data_ptr())
+    return (a, b, b1, d, e, ws), ch, kc, t
+
+
+def main(argv):
+    lib = nat.load()
+    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
+    sel = [a for a in argv if a in SHAPES] or ["gpt67b", "llama"]
+    variant = next((int(a.split("=")[1], 0) for a in argv if a.startswith("variant=")), 0)
+    lib.ff_set_variant(variant)
+    xchg = 0 if 'x0' in argv else (1 if 'x1' in argv else 2)
+    for name in sel:
+        keep, ch, kc, t = setup(*SHAPES[name], xchg, lib)
+        ws = keep[-1]
+
+        def f():
+            nat.check(lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(kc), ctypes.byref(t), ws.data_ptr(),
+                                          ws.numel(), None))
+        buf = torch.zeros(kc.grid_ctas * ST + 64, dtype=torch.int64, device='cuda')
+        for _ in range(3):
+            f()
+        runs = []
+        for _ in range(5):
+            if 'warm' not in argv:
+                flush_buf.add_(1.0)
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            buf.zero_()
+            lib.ff_set_profile_buffer(ctypes.c_void_p(buf.data_ptr()))
+            ea.record()
+            f()
+            eb.record()
+            lib.ff_set_profile_buffer(None)
+            torch.cuda.synchronize()
+            v = buf[:kc.grid_ctas * ST].view(kc.grid_ctas, ST)[:, 16:].double()
+            runs.append((ea.elapsed_time(eb) * 1e3, v.clone()))
+        runs.sort(key=lambda r: r[0])
+        us, v = runs[2]
+        valid = v[:, 0] > 0
+        v = v[valid]
+        rel = (v - v[:, 0].min()) / 1e3
+        rel[v == 0] = float('nan')
+        print(f"== {name} variant {variant:#x} {kc.as_dict()}: events {us:.1f} us, active CTAs {int(valid.sum())}")
+        for i in range(16):
+            col = rel[:, i]
+            col = col[~torch.isnan(col)]
+            if col.numel():
+                print(f"   {NAMES[i]:11s} min {col.min().item():7.1f} mean {col.mean().item():7.1f} "
+                      f"max {col.max().item():7.1f} us")
+        if 'rings' in argv:
+            g2 = kc.ring * 2
+            for r in range(kc.rings):
+                blk = rel[r * g2:(r + 1) * g2]
+                cols = {k: blk[:, i] for i, k in ((2, 'cfull0'), (5, 'cfull1'), (14, 'E_start'), (15, 'exit'))}
+                print("   ring %d: " % r + " ".join(
+                    f"{k} {c[~torch.isnan(c)].mean().item():6.1f}/{c[~torch.isnan(c)].max().item():6.1f}"
+                    for k, c in cols.items()))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
+    nat.load().ff_set_variant(0)
