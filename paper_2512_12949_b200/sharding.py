@@ -61,7 +61,7 @@ def run_sharded(graph: ChainGraph, tensors: dict, group=None, gather: bool = Fal
     local = a if a.shape[0] == hi - lo else a[lo:hi]
     sub = shard_graph(graph, world, rank)
     if sub is None:
-        out = torch.empty((0, graph.dims.l), dtype=torch.bfloat16, device=a.device)
+        out = torch.empty((0, graph.dims.l), dtype=a.dtype, device=a.device)
     else:
         shard = dict(tensors)
         if sub.dims.m != local.shape[0]:  # pad tiny shards up to one row granule
@@ -76,6 +76,11 @@ def run_sharded(graph: ChainGraph, tensors: dict, group=None, gather: bool = Fal
     # a GPU in tests) gathers host copies
     on_host = dist.get_backend(group) == "gloo"
     dev = torch.device("cpu") if on_host else out.device
-    parts = [torch.empty((h - l_, graph.dims.l), dtype=out.dtype, device=dev) for l_, h in sizes]
-    dist.all_gather(parts, out.contiguous().to(dev), group=group)
-    return torch.cat(parts).to(out.device)
+    # all_gather wants equal-sized parts (gloo enforces it): shards differ by at most one
+    # row granule, so every rank sends its rows padded to the largest shard
+    rows = max(h - l_ for l_, h in sizes)
+    send = torch.zeros((rows, graph.dims.l), dtype=out.dtype, device=dev)
+    send[: out.shape[0]] = out.to(dev)
+    parts = [torch.empty_like(send) for _ in sizes]
+    dist.all_gather(parts, send, group=group)
+    return torch.cat([p[: h - l_] for p, (l_, h) in zip(parts, sizes)]).to(out.device)

@@ -78,3 +78,43 @@ def test_gloo_world2_sharded_chain_equals_unsharded():
     for rank, err, tmax in results:
         assert err <= 1e-4
         assert tmax == 2.0
+
+
+def _run_sharded_worker(rank, world, port, m, q):
+    """sharding.run_sharded itself (row split, tiny-shard padding, all-gather of
+    ragged shards) with the chain launch replaced by a row-wise host function:
+    no GPU here, and the gather logic is what is under test."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_12949_b200 import runtime
+
+        w = torch.arange(32 * 24, dtype=torch.float32).reshape(32, 24) / 100.0
+        runtime.run = lambda graph, plan, t, exchange="auto": t["A"] @ w  # row-wise, like the chain
+        graph = W.build_standard_ffn(W.DimensionSpec(m, 64, 32, 24), "relu")
+        a = torch.randn(m, 32, generator=torch.Generator().manual_seed(1))
+        mine = sharding.run_sharded(graph, {"A": a})
+        full = sharding.run_sharded(graph, {"A": a}, gather=True)
+        lo, hi = sharding.shard_bounds(m, world, rank)
+        q.put((rank, tuple(mine.shape), bool(torch.equal(mine, (a @ w)[lo:hi])),
+               bool(torch.equal(full, a @ w)), None))
+    except Exception as exc:
+        q.put((rank, None, None, None, repr(exc)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,world", [(1040, 2), (48, 4)])
+def test_run_sharded_gathers_ragged_shards(m, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_sharded_worker, args=(r, world, port, m, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, shape, same_rows, same_full, exc in results:
+        assert exc is None, exc
+        lo, hi = sharding.shard_bounds(m, world, rank)
+        assert shape == (hi - lo, 24) and same_rows and same_full
