@@ -379,7 +379,7 @@ def choose_config(name, tensors, profile=True, m=None, flush=None):
 
     plans = _plans_of(name, m)
     cands = {}  # config key -> [cfg, labels, plan]
-    for plan, x in [(p, x) for p in plans for x in ("pair", "l2", "dsm")] + [(None, x) for x in ("pair", "l2", "dsm")]:
+    for plan, x in [(p, x) for p in plans for x in ("pair", "l2", "dsm", "l2dsm")] + [(None, x) for x in ("pair", "l2", "dsm", "l2dsm")]:
         try:
             cfg = runtime.lower(graph, plan, 148, x)
         except Exception:

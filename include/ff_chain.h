@@ -80,6 +80,9 @@ typedef struct ffPlanDesc {
 #define FF_XCHG_DSM 0 /* distributed shared memory pushes inside a thread-block cluster */
 #define FF_XCHG_L2 1  /* TMA store / TMA load through an L2-resident scratch (cooperative launch) */
 #define FF_XCHG_L2_PAIR 2 /* as FF_XCHG_L2, ring members are CTA pairs issuing cta_group::2 M=256 MMAs */
+#define FF_XCHG_L2_DSMR 3 /* as FF_XCHG_L2 (1-CTA members), and the n_splits (2..8) N splits of every E tile
+                             form one thread-block cluster that sums their fp32 partials by a DSM
+                             reduce-scatter (the paper's dsm_comm reduce_scatter); one unit per ring */
 
 /* Physical launch configuration produced by the lowering. */
 typedef struct ffKernelConfig {
@@ -87,7 +90,7 @@ typedef struct ffKernelConfig {
   int32_t n_splits;    /* N splits whose E partials are reduced across rings (inter-cluster reduce) */
   int32_t nb;          /* C chunk width per CTA per n-step (columns) */
   int32_t lb;          /* E columns owned by one CTA (TMEM accumulator width) */
-  int32_t exchange;    /* FF_XCHG_DSM | FF_XCHG_L2 */
+  int32_t exchange;    /* FF_XCHG_DSM | FF_XCHG_L2 | FF_XCHG_L2_PAIR | FF_XCHG_L2_DSMR */
   int32_t m_tiles;     /* derived: ceil(m / 128) */
   int32_t l_clusters;  /* derived: l / (ring * lb) */
   int32_t steps;       /* derived: n-steps per split */
@@ -189,6 +192,8 @@ void ff_set_profile_buffer(void* dev_ptr);
 #define FF_VARIANT_WEIGHTS_EVICT_FIRST 0x10u /* pair kernel: weight tiles + prefetches with L2 evict_first */
 #define FF_VARIANT_SCRATCH_NORMAL 0x20u      /* pair kernel: C exchange scratch with the default L2 priority */
 #define FF_VARIANT_WEIGHTS_EVICT_LAST 0x40u  /* pair kernel: weight tiles + prefetches with L2 evict_last */
+#define FF_VARIANT_NO_DISCARD 0x80u          /* pair kernel: keep dead exchange scratch in L2 (no discard) */
+#define FF_VARIANT_NO_SCRATCH_DISCARD 0x100u /* pair kernel: discard only the split-N exchange regions */
 void ff_set_variant(uint32_t flags);
 
 /* Thread-local message for the last non-OK status. */

@@ -26,7 +26,7 @@ FF_ERR_ARG = 5
 KIND = {"standard_ffn": 0, "gated_ffn": 1}
 ACT = {"identity": 0, "relu": 1, "silu": 2, "gelu": 3}
 LOWERING = {"n/a": 0, "spatial_split": 1, "doubled_k": 2}
-XCHG_DSM, XCHG_L2, XCHG_L2_PAIR = 0, 1, 2
+XCHG_DSM, XCHG_L2, XCHG_L2_PAIR, XCHG_L2_DSMR = 0, 1, 2, 3  # ff_chain.h FF_XCHG_*
 DTYPE = {"bf16": 0, "f16": 1}
 
 # Exported symbols (must match include/ff_chain.h).

@@ -239,8 +239,9 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // (split_finish), and no config puts C scratch inside them, so a workspace
 // zero-filled once stays valid whatever configs share it.  A split chain whose
 // fp32 E exceeds the zone spills past it and clears it with a memset first.
-// flag region (u32 words): [0, 2^17) ring chunk-ready flags, [2^17, 2^18) split-N slab
-// flags; its last word holds the device epoch
+// flag region (u32 words): [0, 2^17) ring chunk-ready flags, [2^17, 3*2^16) split-N slab
+// flags, [3*2^16, 2^18 - 1) the pair kernel's per-(ring, member) "done reading the C
+// scratch" flags; its last word holds the device epoch
 constexpr size_t kFlagBytes = 1u << 20;
 constexpr size_t kRingFlagBytes = 512u << 10;
 constexpr size_t kCntBytes = 256u << 10;
@@ -259,7 +260,8 @@ int pair_c_slots(const ffKernelConfig* c) {
 WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = false) {
   WsLayout w{};
   const bool pair = c->exchange == FF_XCHG_L2_PAIR;
-  const size_t e_bytes = c->n_splits > 1 ? (size_t)ch->m * ch->l * sizeof(float) : 0;
+  const bool dsmr = c->exchange == FF_XCHG_L2_DSMR;  // split partials meet in DSM: no fp32 E, no slab
+  const size_t e_bytes = c->n_splits > 1 && !dsmr ? (size_t)ch->m * ch->l * sizeof(float) : 0;
   // C scratch: L2 transport with a ring > 1; the standard-FFN pair kernel also
   // reads its own chunk back from it (hop 0), so it always needs one.
   // (a k2 x k2 second convolution reads the whole intermediate back through im2col boxes)
@@ -282,7 +284,7 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   }
   // pair kernel split-N reduce-scatter: one fp32 [M][L] slab per split (no zero invariant)
   w.s_off = off;
-  if (c->n_splits > 1)  // split-N exchange regions (pair kernel, and the 1-CTA kernels' final units)
+  if (c->n_splits > 1 && !dsmr)  // split-N exchange regions (pair kernel, and the 1-CTA kernels' final units)
     off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * (pair ? 256 : 128) * ch->l * sizeof(float));
   w.total = off;
   return w;
@@ -295,7 +297,7 @@ uint32_t g_variant = 0;  // kernel-variant selection for A/B runs and tests (ff_
 // with 8-row slices, and the slab flags of every E tile fit their region.
 bool pair_finish_regions(const ffChainDesc* ch, const ffKernelConfig* c, int rings) {
   return c->n_splits > 1 && c->n_splits <= 8 && c->units <= rings && 128 % c->n_splits == 0 &&
-         (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 < (1u << 17);
+         (128 / c->n_splits) % 8 == 0 && (size_t)((ch->m + 255) / 256) * 2 * (ch->l / 256) * 16 < (1u << 16);
 }
 
 template <bool kGated, int kNB, int kLB, int kMode>
@@ -382,7 +384,30 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   cudaLaunchAttribute attr[2];
   int nattr = 0;
   int rings;
-  if (kMode == ff::XCHG_DSM) {
+  const bool split_cl = cfg->exchange == FF_XCHG_L2_DSMR;
+  if (split_cl) {
+    // the S N splits of an E tile form one cluster (their fp32 partials meet in DSM): every
+    // (tile, member) cluster must be co-resident, one unit per ring
+    const int S = cfg->n_splits;
+    attr[nattr].id = cudaLaunchAttributeClusterDimension;
+    attr[nattr].val.clusterDim.x = S;
+    attr[nattr].val.clusterDim.y = 1;
+    attr[nattr].val.clusterDim.z = 1;
+    ++nattr;
+    lc.gridDim = dim3(S, 1, 1);
+    lc.attrs = attr;
+    lc.numAttrs = nattr;
+    int active = 0;
+    if (cudaOccupancyMaxActiveClusters(&active, kern, &lc) != cudaSuccess || active <= 0) {
+      cudaGetLastError();
+      active = table_active_clusters(S, num_sms_cached());
+    }
+    if ((int64_t)cfg->units * cfg->ring > (int64_t)active * S)
+      return fail(FF_ERR_UNSUPPORTED, "DSM reduce-scatter: (tile, member) clusters exceed co-residency");
+    if ((size_t)128 * kLB * 4 > (size_t)C::kOFF_OWN)
+      return fail(FF_ERR_UNSUPPORTED, "DSM reduce-scatter: E tile larger than the pipeline stages");
+    rings = cfg->units;
+  } else if (kMode == ff::XCHG_DSM) {
     attr[nattr].id = cudaLaunchAttributeClusterDimension;
     attr[nattr].val.clusterDim.x = cfg->ring;
     attr[nattr].val.clusterDim.y = 1;
@@ -432,13 +457,14 @@ int launch_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTensor
   a.f16 = ch->dtype == FF_DTYPE_F16 ? 1 : 0;
   a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;
   a.slab = reinterpret_cast<float*>(wsb + wl.s_off);
+  a.split_cl = split_cl ? 1 : 0;
   // final-unit split-N reduce-scatter through exchange regions (FF_VARIANT_FINISH_REGIONS, opt-in): one
   // unit per ring, 8-row slices, the S slots (the whole fp32 tile) in the drained stages
   // and the bf16 row slice in the own slot.  Measured slower than the TMA reduce-add +
   // last-arriver finish for GPT-2s (29.7 vs 26.6 us, profiles/r01/timeline_gpt2s_regions.log):
   // with S = 8 both move ~11-13 MB of fp32 partials into a dirty L2 at once, and the
   // region path adds the partner loads
-  a.finish_tma = S > 1 && S <= 8 && 128 % S == 0 && R % 8 == 0 && cfg->units <= rings && !conv2 &&
+  a.finish_tma = !split_cl && S > 1 && S <= 8 && 128 % S == 0 && R % 8 == 0 && cfg->units <= rings && !conv2 &&
                  (size_t)128 * kLB * 4 <= (size_t)C::kOFF_OWN && (size_t)R * kLB * 2 <= (size_t)C::kCHUNK_BYTES &&
                  (size_t)cfg->m_tiles * (L / kLB) * 16 < (1u << 17) && (g_variant & FF_VARIANT_FINISH_REGIONS);
   if (implicit || conv2) {
@@ -678,6 +704,9 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
               : (g_variant & FF_VARIANT_WEIGHTS_EVICT_LAST) ? ff::L2_EVICT_LAST
                                                             : ff::L2_NORMAL;
   a.cpolicy = (g_variant & FF_VARIANT_SCRATCH_NORMAL) ? ff::L2_NORMAL : ff::L2_EVICT_LAST;
+  // dead scratch leaves L2 without a DRAM write-back (FF_VARIANT_NO_DISCARD: keep it)
+  a.discard = (g_variant & FF_VARIANT_NO_DISCARD) ? 0 : (g_variant & FF_VARIANT_NO_SCRATCH_DISCARD) ? 1 : 3;
+  a.cscratch = reinterpret_cast<__nv_bfloat16*>(wsb + wl.c_off);
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));
@@ -764,7 +793,7 @@ LaunchFn select_kernel(bool gated, int nb, int lb, int mode) {
 #define FF_CASE(G, NB, LB)                                                    \
   if (gated == G && nb == NB && lb == LB)                                     \
     return mode == FF_XCHG_DSM ? &launch_impl<G, NB, LB, ff::XCHG_DSM>        \
-                               : &launch_impl<G, NB, LB, ff::XCHG_L2>;
+                               : &launch_impl<G, NB, LB, ff::XCHG_L2>; /* L2 and L2_DSMR */
   FF_CASE(false, 128, 256)
   FF_CASE(false, 128, 128)
   FF_CASE(false, 128, 64)
@@ -797,8 +826,11 @@ int validate_chain(const ffChainDesc* ch) {
 // Fill derived fields and check that a physical configuration is executable.
 int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const bool gated = ch->kind == FF_KIND_GATED;
-  if (c->exchange != FF_XCHG_DSM && c->exchange != FF_XCHG_L2 && c->exchange != FF_XCHG_L2_PAIR)
+  if (c->exchange != FF_XCHG_DSM && c->exchange != FF_XCHG_L2 && c->exchange != FF_XCHG_L2_PAIR &&
+      c->exchange != FF_XCHG_L2_DSMR)
     return fail(FF_ERR_ARG, "unknown exchange");
+  if (c->exchange == FF_XCHG_L2_DSMR && (c->n_splits < 2 || c->n_splits > 8 || 128 % c->n_splits))
+    return fail(FF_ERR_UNSUPPORTED, "DSM reduce-scatter needs 2, 4 or 8 N splits (one cluster per E tile)");
   const int width = c->exchange == FF_XCHG_L2_PAIR ? 2 : 1;  // CTAs per ring member
   if (c->ring < 1 || c->ring > (c->exchange == FF_XCHG_DSM ? 16 : num_sms / width))
     return fail(FF_ERR_UNSUPPORTED, "ring size out of range (DSM rings are clusters of <= 16 CTAs)");
@@ -825,6 +857,12 @@ int finish_config(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const int64_t max_rings =
       c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
   c->rings = (int32_t)std::min<int64_t>(units, max_rings);
+  if (c->exchange == FF_XCHG_L2_DSMR) {
+    // every split cluster co-resident at once (one unit per ring, the tiles' S CTAs meet in DSM)
+    if (units * c->ring > (int64_t)table_active_clusters(c->n_splits, num_sms) * c->n_splits)
+      return fail(FF_ERR_UNSUPPORTED, "DSM reduce-scatter needs every (tile, member) cluster co-resident");
+    c->rings = (int32_t)units;
+  }
   c->grid_ctas = c->rings * c->ring * width;
   return FF_OK;
 }
@@ -840,9 +878,12 @@ void fill_machine(const ffChainDesc* ch, ffKernelConfig* c, int num_sms) {
   const int width = c->exchange == FF_XCHG_L2_PAIR ? 2 : 1;
   const int max_rings =
       c->exchange == FF_XCHG_DSM ? table_active_clusters(c->ring, num_sms) : num_sms / (c->ring * width);
+  const bool dsmr = c->exchange == FF_XCHG_L2_DSMR;
+  if (dsmr && c->n_splits < 2 && splits_ok(ch, c, 2)) c->n_splits = 2;  // a split cluster needs >= 2 splits
   for (;;) {
     const int64_t per = (int64_t)((ch->m + 128 * width - 1) / (128 * width)) * (ch->l / ((int64_t)c->ring * c->lb));
     const int64_t next = (int64_t)c->n_splits * 2;
+    if (dsmr && (next > 8 || per * next * c->ring > (int64_t)table_active_clusters((int)next, num_sms) * next)) break;
     if (per * next > max_rings) break;
     if (!splits_ok(ch, c, next)) break;
     c->n_splits = (int32_t)next;
@@ -952,6 +993,8 @@ int ff_plan_lower_ex(const ffChainDesc* ch, const ffPlanDesc* plan, int32_t num_
   const int32_t reduce_sets = (cn * ck) / cl;
   c.n_splits = (int32_t)(grid_n * reduce_sets);
   c.nb = exchange == FF_XCHG_L2_PAIR ? (gated ? 128 : 256) : (gated ? 64 : 128);
+  if (exchange == FF_XCHG_L2_DSMR)
+    while (c.n_splits > 8) c.n_splits /= 2;  // one portable cluster of split partners
   while (c.n_splits > 1 && !splits_ok(ch, &c, c.n_splits)) c.n_splits /= 2;
   if (!splits_ok(ch, &c, c.n_splits) && exchange != FF_XCHG_L2_PAIR) c.nb = 64;
   if (!splits_ok(ch, &c, c.n_splits)) return fail(FF_ERR_UNSUPPORTED, "n cannot be partitioned into ring chunks");

@@ -75,6 +75,11 @@ struct ChainArgs {
   int c_slots;         // pair kernel: C exchange slots per ring member (scratch reused every c_slots n-steps)
   int wpolicy;         // pair kernel: L2 hint (L2Hint) for weight tiles and their L2 prefetches
   int cpolicy;         // pair kernel: L2 hint for the C exchange scratch (stores and loads)
+  int split_cl;        // L2 kernels: the S N splits of an E tile are one thread-block cluster and combine
+                       // their fp32 partials by a DSM reduce-scatter (FF_XCHG_L2_DSMR)
+  int discard;         // pair kernel: drop dead scratch from L2 without a DRAM write-back once its last
+                       // reader is done: bit 0 the split-N exchange regions, bit 1 the C scratch
+  __nv_bfloat16* cscratch;  // pair kernel: C exchange scratch base (row-major [regions * 256][kN0])
   // conv chain as implicit GEMM (conv_k1 > 1): A is an NHWC feature map read
   // through an im2col tensor map; GEMM0 k-block kb = (filter tap, 64-channel block)
   int conv_k1;         // filter size of the first convolution (0: plain A[M][K])
@@ -285,8 +290,12 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) FF_STAMP(16);
   const int warp = threadIdx.x / 32;
   const int G = args.G;
-  const uint32_t p = kDSM ? cluster_rank() : (uint32_t)(blockIdx.x % G);  // ring position
-  const int ring = blockIdx.x / G;
+  // split clusters (FF_XCHG_L2_DSMR): CTA x = ((tile * G) + p) * S + split, cluster rank = split;
+  // ring = tile + split * (m_tiles * l_clusters), so unit_of(0) of rank s is split s of the tile
+  const int Sc = args.split_cl ? args.S : 1;
+  const uint32_t p = kDSM ? cluster_rank() : (uint32_t)((blockIdx.x / Sc) % G);  // ring position
+  const int ring = args.split_cl ? (int)(blockIdx.x / (Sc * G)) + (int)(blockIdx.x % Sc) * args.m_tiles * args.l_clusters
+                                 : (int)(blockIdx.x / G);
   const int kblocks = args.K / C::BK;
   // GEMM0 k order rotated by ring position (members of a ring and the rings of
   // an m tile would otherwise request the same A box at the same moment)
@@ -713,6 +722,7 @@ __global__ void __launch_bounds__(256, 1)
         // is free (hop 0 read it, pushes acked / C store done)
         const bool final_unit = (T / steps) == my_units - 1;
         const bool issuer = (warp == 4 && lane_id() == 0);
+        if (args.split_cl) continue;  // one unit per ring: the DSM reduce-scatter below (all warps)
         if (final_unit && args.finish_tma) {
           // Split-N reduce-scatter through exchange regions (as the pair kernel's tail):
           // row slice j (R = 128/S rows) of the E tile belongs to split j; rows of other
@@ -891,6 +901,69 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
 
+  if (!kDSM && args.split_cl && total_steps > 0) {
+    // ============ split-N DSM reduce-scatter (all 8 warps, FF_XCHG_L2_DSMR) ============
+    // The paper's dsm_comm reduce_scatter (analyzer.py:348, simulator.py:363-367) on the
+    // S fp32 E partials of one tile, one per CTA of the cluster: row slice j (R = 128/S
+    // rows) belongs to cluster rank j.  Every thread takes half of one row's columns from
+    // TMEM and stores them with st.shared::cluster into the owner's drained pipeline
+    // stages, slot [source split][R rows][kLB], 16-byte chunks XOR-swizzled by row (8
+    // consecutive rows of a warp hit distinct bank groups).  After a cluster barrier each
+    // CTA sums the S partials of its rows in split order (deterministic, bit-reproducible),
+    // casts and writes its E rows: no fp32 workspace, no flags, no atomics.
+    const int S = args.S, R = C::BM / S;
+    const Unit u = unit_of(my_units - 1);
+    const int sp = (int)cluster_rank();
+    const int wq = warp & 3;
+    const int row = wq * 32 + (int)lane_id();
+    const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
+    const int c_lo = warp < 4 ? kLB / 2 : 0;
+    mbar_wait(e_full, (my_units - 1) & 1);
+    __syncwarp();
+    tc_fence_after();
+    if (threadIdx.x == 128) FF_STAMP(30);
+    cluster_sync();  // every CTA's MMAs retired: all stage areas are free to receive
+    const uint32_t dst_rank = (uint32_t)(row / R);
+    const uint32_t dst_row = base + (uint32_t)((sp * R + row % R) * kLB * 4);
+    const uint32_t rdst = dst_rank == (uint32_t)sp ? dst_row : mapa(dst_row, dst_rank);
+#pragma unroll 1
+    for (int c0 = c_lo; c0 < c_lo + kLB / 2; c0 += 32) {
+      float v[32];
+      tmem_ld32(lane_base + C::kTMEM_E + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t a = rdst + ((((c0 / 4 + j) ^ (row & 7))) << 4);
+        if (dst_rank == (uint32_t)sp)
+          st_shared_v4(a, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                       __float_as_uint(v[4 * j + 3]));
+        else
+          st_cluster_v4(a, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                        __float_as_uint(v[4 * j + 3]));
+      }
+    }
+    cluster_sync();  // partials of this CTA's rows have landed (release / acquire at cluster scope)
+    if (threadIdx.x == 128) FF_STAMP(24);
+    constexpr int kChunks = kLB / 4;  // 16-byte chunks per row
+    const int rows_here = min(R, args.M - (u.m0 + sp * R));
+#pragma unroll 1
+    for (int it = (int)threadIdx.x; it < R * kChunks; it += 256) {
+      const int rr = it / kChunks, c = it % kChunks;
+      if (rr >= rows_here) break;
+      const uint32_t off = (uint32_t)(rr * kLB * 4) + (((c ^ (rr & 7))) << 4);
+      float4 a = ld_shared_f4(base + off);
+#pragma unroll 1
+      for (int j = 1; j < S; ++j) {  // splits in order
+        const float4 f = ld_shared_f4(base + (uint32_t)(j * R * kLB * 4) + off);
+        a.x += f.x;
+        a.y += f.y;
+        a.z += f.z;
+        a.w += f.w;
+      }
+      const size_t e_off = (size_t)(u.m0 + sp * R + rr) * args.L + u.l0 + 4 * c;
+      *reinterpret_cast<uint2*>(args.E + e_off) = make_uint2(pack2(args.f16, a.x, a.y), pack2(args.f16, a.z, a.w));
+    }
+    if (threadIdx.x == 128) FF_STAMP(26);
+  }
   __syncthreads();
   if (kDSM) cluster_sync();  // no CTA leaves while a peer may still push or credit
   if (threadIdx.x == 0) FF_STAMP(31);

@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(256, 1)
   // Split-N reduce-scatter tail (one unit per ring, S > 1): all eight warps
   // drain the ring's last E partial after the role loops (see below).
   const bool scatter_all = args.S > 1 && args.finish_tma && total_steps > 0;
+  // C scratch discard at exit (one set of regions per ring, addressed per member and slot)
+  const bool discard_c = (args.discard & 2) && !kRagged && (G > 1 || !C::kOwnFull) && my_units > 0;
+  auto done_flag = [&](int member) { return args.flags + (3u << 16) + ring * G + member; };
   // A tile: two K-major [128 x 64] SW128 tiles; B tile: MN-major [128 k x 64] tiles 16 KB apart
   auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
   auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
@@ -436,6 +439,9 @@ __global__ void __launch_bounds__(256, 1)
           hop(T, h);
         }
       }
+      // every C load of this pair has landed (its full barriers completed): the ring's
+      // scratch is no longer read by this member
+      if (discard_c) st_release_gpu_u32(done_flag(p), epoch);
       if (args.prof) {
         unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
         pr[3] = clock64() - t_start;
@@ -785,6 +791,15 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(e_load, 0);
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
+    if (args.discard & 1) {  // the partners' rows of this slice are read exactly once: drop them from L2
+      const int lines = kChunks * R / 8;  // 128-byte lines of one (region, slice) block
+      for (int j = 0; j < S; ++j) {
+        if (j == sp) continue;
+        const uint8_t* blk = reinterpret_cast<const uint8_t*>(region(j)) + sp * R * 16;
+        for (int i = tid; i < lines; i += 256)
+          discard_l2_line(blk + (size_t)(i / (R / 8)) * 2048 + (i % (R / 8)) * 128);
+      }
+    }
     // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
     const uint8_t* const src = smem_gen;
     const int n_items = R * kChunks;
@@ -827,6 +842,27 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
 
+  if (discard_c) {
+    // once every member of the ring has read its last chunk, drop this CTA's half of its own
+    // chunk regions (c_slots x 128 rows x kN0 columns) from L2 instead of writing them back;
+    // the done flags were published right after the members' last hops, long before their
+    // tails end, so the poll finds them set
+    if (warp == 2) {
+      uint32_t polls = 0;
+      for (int j = (int)lane_id(); j < G; j += 32)
+        while (ld_relaxed_gpu_u32(done_flag(j)) != epoch)
+          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+      fence_acq_rel_gpu();
+    }
+    __syncthreads();
+    constexpr int kRowLines = C::kN0 * 2 / 128;
+    const int lines = args.c_slots * C::BM * kRowLines;
+    for (int i = (int)threadIdx.x; i < lines; i += 256) {
+      const int slot = i / (C::BM * kRowLines), r = (i / kRowLines) % C::BM, c = i % kRowLines;
+      const size_t row = (size_t)((ring * G + p) * args.c_slots + slot) * (2 * C::BM) + (int)q * C::BM + r;
+      discard_l2_line(reinterpret_cast<const uint8_t*>(args.cscratch) + row * (C::kN0 * 2) + c * 128);
+    }
+  }
   __syncthreads();
   cluster_sync();
   if (threadIdx.x == 0) FF_STAMP(31);

@@ -168,6 +168,11 @@ __device__ __forceinline__ uint32_t ld_relaxed_gpu_u32(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Invalidate one 128-byte L2 line without writing it back (scratch whose last reader is
+// done: its dirty lines would otherwise cost a DRAM write-back after the kernel).
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 // named barrier among `count` threads
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
@@ -616,6 +621,11 @@ __device__ __forceinline__ uint32_t pack2(bool f16, float lo, float hi) {
 // instruction descriptor of a bf16 MMA switched to fp16 A/B (kind::f16: format 0 = f16, 1 = bf16)
 __host__ __device__ constexpr uint32_t idesc_as(uint32_t idesc, bool f16) {
   return f16 ? (idesc & ~((1u << 7) | (1u << 10))) : idesc;
+}
+// 16-byte store into another CTA's shared memory (address from mapa)
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared::cluster.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
 }
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)

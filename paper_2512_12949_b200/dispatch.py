@@ -99,33 +99,43 @@ class Dispatcher:
             return cls.from_dict(json.load(fh))
 
 
-def candidate_configs(graph, plans=()) -> list:
+def candidate_configs(graph, plans=(), labelled: bool = False) -> list:
     """Distinct lowerings of the runtime's auto configuration under every
-    transport, plus the given plans' lowerings (no GPU needed)."""
+    transport, plus the given plans' lowerings (no GPU needed).  labelled: (cfg,
+    [sources]) pairs, a source per plan / transport that lowers to the config."""
     from . import runtime
 
-    seen, out = set(), []
-    sources = [(None, x) for x in ("pair", "l2", "dsm")] + [(p, x) for p in plans for x in ("pair", "l2", "dsm")]
-    for plan, x in sources:
+    seen, out = {}, []
+    xs = ("pair", "l2", "dsm", "l2dsm")
+    sources = [(None, -1, x) for x in xs] + [(p, j, x) for j, p in enumerate(plans) for x in xs]
+    for plan, j, x in sources:
         try:
             cfg = runtime.lower(graph, plan, 148, x)
         except nat.UnsupportedPlan:
             continue
         key = tuple(int(getattr(cfg, f)) for f in _FIELDS)
-        if key not in seen:
-            seen.add(key)
-            out.append(cfg)
-    return out
+        label = f"runtime-auto [{x}]" if plan is None else f"searched #{j} {plan.describe()} [{x}]"
+        if key in seen:
+            seen[key][1].append(label)
+        else:
+            seen[key] = (cfg, [label])
+            out.append(seen[key])
+    return out if labelled else [c for c, _ in out]
 
 
 def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT_BINS, iters: int = 10,
                 warmup: int = 3, seed: int = 0, plans_by_m: Optional[dict] = None) -> Dispatcher:
     """Profile every candidate launch at each bin's upper edge (L2 flushed
-    between timed launches) and keep the fastest: ProfileBestFromList per bin."""
+    between timed launches) and keep the fastest: ProfileBestFromList per bin.
+    Candidates: the runtime's lowerings under every transport plus the lowerings of
+    the reference search's top-K plans for that M (plans_by_m, default: the
+    shipped plans/plan_bins.json -- the offline-search leg, PAPER.md SIV-C3)."""
     import torch
 
-    from . import runtime
+    from . import plan_cache, runtime
 
+    if plans_by_m is None:
+        plans_by_m = plan_cache.plans_by_m(kind, activation, n, k, l, bins)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     gen = torch.Generator(device="cpu").manual_seed(seed)
 
@@ -144,7 +154,8 @@ def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT
         tensors = dict(weights, A=u(m, k))
         out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
         timed = []
-        for cfg in candidate_configs(graph, (plans_by_m or {}).get(m, ())):
+        plans = plans_by_m.get(m, ())
+        for cfg, labels in candidate_configs(graph, plans, labelled=True):
             for _ in range(warmup):
                 runtime.launch(graph, cfg, tensors, out=out)
             ts = []
@@ -156,14 +167,20 @@ def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT
                 b.record()
                 b.synchronize()
                 ts.append(a.elapsed_time(b))
-            timed.append((sorted(ts)[len(ts) // 2], cfg))
-        ms, best = min(timed, key=lambda x: x[0])
+            timed.append((sorted(ts)[len(ts) // 2], cfg, labels))
+        timed.sort(key=lambda x: x[0])
+        ms, best, labels = timed[0]
         entry = {f: int(getattr(best, f)) for f in _FIELDS}
         entry["ms"] = round(ms, 5)
         entry["candidates"] = len(timed)
+        entry["searched_plans"] = len(plans)
+        entry["won_by"] = labels
+        entry["timed"] = [[round(t * 1e3, 2), " = ".join(lb)] for t, _, lb in timed]
         configs.append(entry)
     return Dispatcher(kind, activation, n, k, l, list(bins), configs,
-                      {"device": torch.cuda.get_device_name(), "method": "median of %d cold-L2 launches" % iters})
+                      {"device": torch.cuda.get_device_name(), "method": "median of %d cold-L2 launches" % iters,
+                       "candidates": "runtime lowerings (pair / l2 / dsm) + lowerings of the reference search's "
+                                     "top-K plans per M bin (plans/plan_bins.json)"})
 
 
 # BASELINE.json families shipped with the package (plans/dispatch/*.json)

@@ -16,6 +16,9 @@ from .workload import DimensionSpec, build_gated_ffn, build_standard_ffn
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CACHE = os.path.join(HERE, "plans", "plan_cache.json")
+# searched top-K plans per (dispatch family, M bin): the offline-search leg of the M-bin
+# dispatch tables (dispatch.build_table profiles them on the device)
+BINS_CACHE = os.path.join(HERE, "plans", "plan_bins.json")
 
 # (kind, activation class, m, n, k, l): the BASELINE.json configurations.
 SHAPES = [
@@ -65,9 +68,49 @@ def build(shapes=SHAPES, k_top: int = 11, workers: int = 8) -> dict:
     return out
 
 
+def build_bins(families=None, bins=None, k_top: int = 11, workers: int = 8) -> dict:
+    """The reference search's top-K plans (B200 profile) for every dispatch family at
+    the upper edge of every M bin (paper SIV-C3: offline search per M bin)."""
+    from .dispatch import DEFAULT_BINS, FAMILIES
+
+    families = FAMILIES if families is None else families
+    bins = DEFAULT_BINS if bins is None else bins
+    shapes = [(kind, act, m, n, k, l) for kind, act, n, k, l in families.values() for m in bins]
+    return build(shapes, k_top=k_top, workers=workers)
+
+
+_bins = None
+
+
+def plans_by_m(kind, act, n, k, l, bins) -> dict:
+    """{M: [FusionPlan, ...]} from plans/plan_bins.json for one dispatch family
+    (bins without an entry are left out)."""
+    global _bins
+    from .plan import plan_from_dict
+
+    if _bins is None:
+        _bins = {}
+        if os.path.exists(BINS_CACHE):
+            with open(BINS_CACHE) as fh:
+                _bins = json.load(fh)
+    out = {}
+    for m in bins:
+        e = _bins.get(_key(kind, act, m, n, k, l))
+        if e is not None:
+            out[m] = [plan_from_dict(p) for p in e["top"]]
+    return out
+
+
 if __name__ == "__main__":
+    import sys
+
     os.makedirs(os.path.dirname(CACHE), exist_ok=True)
-    doc = build()
-    with open(CACHE, "w") as fh:
+    if "bins" in sys.argv[1:]:
+        doc = build_bins()
+        path = BINS_CACHE
+    else:
+        doc = build()
+        path = CACHE
+    with open(path, "w") as fh:
         json.dump(doc, fh, sort_keys=True, indent=1)
-    print(f"wrote {CACHE}: {len(doc)} shapes")
+    print(f"wrote {path}: {len(doc)} shapes")

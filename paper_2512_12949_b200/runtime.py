@@ -59,7 +59,7 @@ def _num_sms() -> int:
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
-EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2, "pair": nat.XCHG_L2_PAIR}
+EXCHANGES = {"dsm": nat.XCHG_DSM, "l2": nat.XCHG_L2, "pair": nat.XCHG_L2_PAIR, "l2dsm": nat.XCHG_L2_DSMR}
 
 
 def exchange_name(cfg: nat.KernelConfig) -> str:
@@ -72,7 +72,9 @@ def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optiona
     runtime choose the hardware-shaped configuration; ``exchange`` picks the
     shuffle transport: "dsm" (thread-block cluster, distributed shared memory),
     "l2" (TMA through an L2-resident scratch), "pair" (L2 transport, CTA-pair
-    cta_group::2 kernel) or "auto" (first of pair, l2, dsm that supports it)."""
+    cta_group::2 kernel), "l2dsm" (L2 ring; the N splits of every E tile form a
+    thread-block cluster and reduce their partials over DSM) or "auto" (first of
+    pair, l2, dsm that supports it)."""
     if exchange == "auto":
         last = None
         for candidate in ("pair", "l2", "dsm"):

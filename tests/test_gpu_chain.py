@@ -66,7 +66,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair", "l2dsm"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
 def test_fused_chain_matches_oracle(case, exchange):
     from paper_2512_12949_b200 import _native as nat
@@ -269,7 +269,7 @@ def _random_cases(n, seed):
     return cases
 
 
-@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair", "l2dsm"])
 @pytest.mark.parametrize("case", _random_cases(10, 2025), ids=lambda c: f"{c[0][:3]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
 def test_random_shapes_match_oracle(case, exchange):
     """Seeded random shapes (ragged M down to 16, K in 128s, N/L in 256s) under every transport."""
@@ -357,7 +357,7 @@ def test_workspace_zero_invariant_across_configs():
     seq = [("gated_ffn", "silu", 128, 3328, 256, 1792), ("standard_ffn", "relu", 200, 768, 256, 768),
            ("gated_ffn", "silu", 384, 768, 1536, 1792), ("standard_ffn", "gelu", 512, 3072, 768, 768)]
     for case in seq:
-        for exchange in ("pair", "l2", "dsm"):
+        for exchange in ("pair", "l2", "dsm", "l2dsm"):
             graph = _graph(*case)
             try:
                 cfg = runtime.lower(graph, None, 148, exchange)
@@ -380,7 +380,7 @@ F16_CASES = [
 ]
 
 
-@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair"])
+@pytest.mark.parametrize("exchange", ["dsm", "l2", "pair", "l2dsm"])
 @pytest.mark.parametrize("case", F16_CASES, ids=lambda c: f"{c[0][:3]}-{c[1]}-{c[2]}x{c[3]}x{c[4]}x{c[5]}")
 def test_fp16_chain_matches_oracle(case, exchange):
     """fp16 storage (north star: bf16/fp16 with fp32 accumulation).  Weights are
@@ -431,6 +431,33 @@ def test_one_cta_region_finish_matches_oracle_and_repeats_bitwise(case, exchange
         torch.cuda.synchronize()
     finally:
         lib.ff_set_variant(0)
+    _check(kind, act, host, out1)
+    assert torch.equal(out1, out2)
+
+
+@pytest.mark.parametrize("splits", [2, 4, 8])
+@pytest.mark.parametrize("case", [("standard_ffn", "gelu", 512, 3072, 768, 768), ("gated_ffn", "silu", 256, 1024, 512, 512),
+                                  ("standard_ffn", "relu", 200, 2048, 256, 512)],
+                         ids=["gpt2s", "gated-small", "ragged-m"])
+def test_dsm_reduce_scatter_matches_oracle_and_repeats_bitwise(case, splits):
+    """FF_XCHG_L2_DSMR: the N splits of an E tile form one thread-block cluster and sum
+    their fp32 partials by a DSM reduce-scatter (st.shared::cluster into the owner's
+    drained stages, split-order sum): matches the oracle and is bit-reproducible."""
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    cfg = runtime.lower(graph, None, 148, "l2dsm")
+    cfg.n_splits = splits
+    host, dev = _inputs(kind, m, n, k, l, seed=13)
+    try:
+        out1 = runtime.launch(graph, cfg, dev).clone()
+    except nat.UnsupportedPlan as exc:
+        pytest.skip(f"{splits} splits do not tile {case}: {exc}")
+    out2 = runtime.launch(graph, cfg, dev)
+    torch.cuda.synchronize()
     _check(kind, act, host, out1)
     assert torch.equal(out1, out2)
 

@@ -98,6 +98,12 @@ def parse(path):
 
 if __name__ == "__main__":
     if sys.argv[1] == "run":
+        # optional variant=0x.. (ff_set_variant: A/B of kernel variants, e.g. 0x80 = no discard)
+        var = next((int(a.split("=")[1], 0) for a in sys.argv[4:] if a.startswith("variant=")), 0)
+        if var:
+            from paper_2512_12949_b200 import _native
+
+            _native.load().ff_set_variant(var)
         run(sys.argv[2], sys.argv[3])
     else:
         print(json.dumps(parse(sys.argv[2])))

@@ -21,6 +21,9 @@ ST = 32
 NAMES = {0: 'entry', 1: 'setup', 2: 'cfull0', 3: 'drained0', 4: 'stored0', 5: 'cfull1', 6: 'E_summed',
          7: 'drained1', 8: 'E_staged', 9: 'E_slabs_out', 10: 'E_finished', 11: 'E_flags_in', 12: 'E_loaded',
          13: 'E_sum0', 14: 'E_start', 15: 'exit'}
+COUNTERS = ['prod_total', 'prod_w_empty', 'prod_w_flag', 'mma_total', 'mma_w_full_g0', 'mma_w_full_hop',
+            'mma_w_cempty', 'mma_w_own', 'mma_w_eempty', 'epi_total', 'epi_w_cfull', 'epi_w_ofree', 'epi_drainC',
+            'epi_store', 'epi_E']
 SHAPES = {"llama": (512, 8192, 2048, 2048, 2, True), "gpt67b": (512, 16384, 4096, 4096, 1, False),
           "opt": (4096, 8192, 2048, 2048, 1, False), "gpt2s": (512, 3072, 768, 768, 3, False)}
 
@@ -50,7 +53,7 @@ def main(argv):
     sel = [a for a in argv if a in SHAPES] or ["gpt67b", "llama"]
     variant = next((int(a.split("=")[1], 0) for a in argv if a.startswith("variant=")), 0)
     lib.ff_set_variant(variant)
-    xchg = 0 if 'x0' in argv else (1 if 'x1' in argv else 2)
+    xchg = 0 if 'x0' in argv else (1 if 'x1' in argv else (3 if 'x3' in argv else 2))
     for name in sel:
         keep, ch, kc, t = setup(*SHAPES[name], xchg, lib)
         ws = keep[-1]
@@ -73,10 +76,10 @@ def main(argv):
             eb.record()
             lib.ff_set_profile_buffer(None)
             torch.cuda.synchronize()
-            v = buf[:kc.grid_ctas * ST].view(kc.grid_ctas, ST)[:, 16:].double()
-            runs.append((ea.elapsed_time(eb) * 1e3, v.clone()))
+            w = buf[:kc.grid_ctas * ST].view(kc.grid_ctas, ST).double()
+            runs.append((ea.elapsed_time(eb) * 1e3, w[:, 16:].clone(), w[:, :16].clone()))
         runs.sort(key=lambda r: r[0])
-        us, v = runs[2]
+        us, v, cnt = runs[2]
         valid = v[:, 0] > 0
         v = v[valid]
         rel = (v - v[:, 0].min()) / 1e3
@@ -88,6 +91,13 @@ def main(argv):
             if col.numel():
                 print(f"   {NAMES[i]:11s} min {col.min().item():7.1f} mean {col.mean().item():7.1f} "
                       f"max {col.max().item():7.1f} us")
+        if 'counters' in argv:  # per-role wait counters (clock64 cycles, FF_TIMED): mean / max over CTAs
+            live = cnt[valid]
+            for i, nm in enumerate(COUNTERS):
+                col = live[:, i]
+                col = col[col > 0]
+                if col.numel():
+                    print(f"   {nm:15s} mean {col.mean().item() / 1e3:9.1f} max {col.max().item() / 1e3:9.1f} kcyc")
         if 'rings' in argv:
             g2 = kc.ring * 2
             for r in range(kc.rings):
