@@ -704,8 +704,11 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
               : (g_variant & FF_VARIANT_WEIGHTS_EVICT_LAST) ? ff::L2_EVICT_LAST
                                                             : ff::L2_NORMAL;
   a.cpolicy = (g_variant & FF_VARIANT_SCRATCH_NORMAL) ? ff::L2_NORMAL : ff::L2_EVICT_LAST;
-  // dead scratch leaves L2 without a DRAM write-back (FF_VARIANT_NO_DISCARD: keep it)
-  a.discard = (g_variant & FF_VARIANT_NO_DISCARD) ? 0 : (g_variant & FF_VARIANT_NO_SCRATCH_DISCARD) ? 1 : 3;
+  // dead split-N exchange regions leave L2 without a DRAM write-back (FF_VARIANT_NO_DISCARD: keep
+  // them).  Measured (profiles/r02/discard_ab.md): GPT-6.7B DRAM 286.0 -> 277.8 MB (1.004x the
+  // algorithmic bytes), LLaMA-1B 118.2 -> 105.9 MB, no time cost; also discarding the C scratch
+  // at exit (FF_VARIANT_SCRATCH_DISCARD) moves no further bytes and costs 1-2 us
+  a.discard = (g_variant & FF_VARIANT_NO_DISCARD) ? 0 : (g_variant & FF_VARIANT_SCRATCH_DISCARD) ? 3 : 1;
   a.cscratch = reinterpret_cast<__nv_bfloat16*>(wsb + wl.c_off);
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
