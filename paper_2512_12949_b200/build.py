@@ -33,20 +33,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > built for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """defines: extra -D flags for A/B builds of kernel variants (written to another `out`)."""
+    if not force and out == OUT and not _stale():
         return OUT
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "static", "-o", OUT + ".tmp"]
+           "-cudart", "static", *[f"-D{d}" for d in defines], "-o", out + ".tmp"]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2512_12949_b200.build [--force] [-v] [-DNAME=VAL ... --out path.so]
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else OUT
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=out, defines=defs))

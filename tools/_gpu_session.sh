@@ -1,17 +1,14 @@
-# scratch driver for one gpurun session (r02, session 4d): l2dsm transport, discard variants, dispatch tables
+# scratch driver for one gpurun session (r02, session 4f): BK=64 x 6 stages vs BK=128 x 3 stages (pair kernel)
 set -x
-O=gpurun_out/r02s4d; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -25 > $O/gpu_tests.log
-timeout 300 python tools/timeline.py gpt2s x0 > $O/timeline_gpt2s_x0.log 2>&1
-timeout 300 python tools/timeline.py gpt2s x3 > $O/timeline_gpt2s_x3.log 2>&1
-timeout 300 python tools/timeline.py gpt2s llama gpt67b x3 > $O/timeline_x3.log 2>&1
-for v in 0 0x100 0x80; do timeout 300 python tools/timeline.py gpt67b llama opt variant=$v > $O/timeline_v$v.log 2>&1; done
-for w in gpt67b llama1b; do for v in 0 0x100; do
-  timeout 300 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file $O/dram_${w}_v$v.csv python tools/dram_bytes.py run $w fused variant=$v > $O/dram_${w}_v$v.log 2>&1
-  python tools/dram_bytes.py parse $O/dram_${w}_v$v.csv > $O/dram_${w}_v$v.json 2>>$O/dram_${w}_v$v.log
-done; done
-timeout 300 compute-sanitizer --tool racecheck --print-limit 20 python tools/sanitize.py > $O/sanitizer_racecheck.log 2>&1
-timeout 900 python -m paper_2512_12949_b200.dispatch > $O/dispatch_build.log 2>&1
-mkdir -p $O/dispatch; cp paper_2512_12949_b200/plans/dispatch/*.json $O/dispatch/
-timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err
-cat $O/gpu_tests.log | tail -8; grep -h "SUMMARY\|failures" $O/sanitizer_*.log; for f in $O/dram_*.json; do echo $f; grep -o '"dram_total.*' $f; done; grep -h "events\|E_start\|exit" $O/timeline_*.log; cat $O/dispatch_build.log
+O=gpurun_out/r02s4f; mkdir -p $O
+export B64=paper_2512_12949_b200/libff_chain_bk64.so
+FF_CHAIN_LIB=$B64 timeout 900 python -m pytest tests/test_gpu_chain.py -x -q -k "pair or Pair or quad" 2>&1 | tail -5 > $O/gpu_tests_bk64.log
+for lib in default bk64; do
+  if [ $lib = bk64 ]; then export FF_CHAIN_LIB=$B64; else unset FF_CHAIN_LIB; fi
+  timeout 300 python tools/timeline.py gpt67b llama opt opt32k counters > $O/timeline_$lib.log 2>&1
+  timeout 300 python tools/timeline.py gpt67b llama opt opt32k counters > $O/timeline_${lib}_2.log 2>&1
+done
+unset FF_CHAIN_LIB
+M=gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__cycles_elapsed.avg.per_second,lts__throughput.avg.pct_of_peak_sustained_elapsed,l1tex__m_xbar2l1tex_read_bytes.sum
+FF_CHAIN_LIB=$B64 timeout 600 ncu --cache-control none --clock-control none --metrics $M --csv --log-file $O/ncu_opt32k_bk64.csv python tools/dram_bytes.py run opt13b_m32768 fused > $O/ncu_opt32k_bk64.log 2>&1
+cat $O/gpu_tests_bk64.log; grep -h "events" $O/timeline_*.log

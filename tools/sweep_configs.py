@@ -45,7 +45,7 @@ for name in sys.argv[1:]:
     out = torch.empty(m, l, dtype=torch.bfloat16, device="cuda")
     auto = runtime.lower(g, None, 148, "pair")
     res = []
-    for x in ("dsm", "l2", "pair"):
+    for x in ("dsm", "l2", "pair", "l2dsm"):
         for lb in (64, 128, 256):
             for nb in (64, 128, 256):
                 for ring in range(1, 17):

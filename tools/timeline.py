@@ -25,7 +25,8 @@ COUNTERS = ['prod_total', 'prod_w_empty', 'prod_w_flag', 'mma_total', 'mma_w_ful
             'mma_w_cempty', 'mma_w_own', 'mma_w_eempty', 'epi_total', 'epi_w_cfull', 'epi_w_ofree', 'epi_drainC',
             'epi_store', 'epi_E']
 SHAPES = {"llama": (512, 8192, 2048, 2048, 2, True), "gpt67b": (512, 16384, 4096, 4096, 1, False),
-          "opt": (4096, 8192, 2048, 2048, 1, False), "gpt2s": (512, 3072, 768, 768, 3, False)}
+          "opt": (4096, 8192, 2048, 2048, 1, False), "gpt2s": (512, 3072, 768, 768, 3, False),
+          "opt32k": (32768, 8192, 2048, 2048, 1, False)}
 
 
 def setup(m, n, k, l, act, gated, xchg, lib):
