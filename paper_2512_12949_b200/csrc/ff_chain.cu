@@ -491,8 +491,7 @@ struct PairStages {
   using Probe = ff::PairCfg<kGated, 256, 1>;
   static constexpr int kFixed = Probe::kSMEM - Probe::kSTAGE - 2 * 8;
   static constexpr int kMax = (232448 - kFixed - 64) / (Probe::kSTAGE + 16);
-  static constexpr int kCap = Probe::BK == 64 ? 6 : 4;
-  static constexpr int value = kMax > kCap ? kCap : kMax;
+  static constexpr int value = kMax > 4 ? 4 : kMax;
 };
 
 template <bool kGated, bool kPacked, bool kQuad, bool kRagged>
@@ -576,26 +575,25 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   const auto BF = elem_type(ch);  // bf16 or fp16 storage
   bool ok = true;
   if (!hit) {
-  constexpr uint32_t BK = C::BK;
   {  // A [M][K] as {64, M, K/64}
     const uint64_t d[3] = {64, M, K / 64}, st[2] = {K * 2, 128};
-    const uint32_t b[3] = {64, 128, BK / 64};
+    const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.a, BF, 3, t->a, d, st, b);
   }
   if (kGated && kPacked) {  // packed [2][K][N] as {64, K, N/64, 2}
     const uint64_t d[4] = {64, K, N / 64, 2}, st[3] = {N * 2, 128, K * N * 2};
-    const uint32_t b[4] = {64, BK, 1, 2};
+    const uint32_t b[4] = {64, 128, 1, 2};
     ok = ok && make_map_nd(&maps.b, BF, 4, t->b, d, st, b);
     maps.b1 = maps.b;
   } else {
     const uint64_t d[3] = {64, K, N / 64}, st[2] = {N * 2, 128};
-    const uint32_t b[3] = {64, BK, kGated ? 1u : 2u};
+    const uint32_t b[3] = {64, 128, kGated ? 1u : 2u};
     ok = ok && make_map_nd(&maps.b, BF, 3, t->b, d, st, b);
     ok = ok && make_map_nd(&maps.b1, BF, 3, kGated ? t->b1 : t->b, d, st, b);
   }
   {  // D [N][L] as {64, N, L/64}
     const uint64_t d[3] = {64, N, L / 64}, st[2] = {L * 2, 128};
-    const uint32_t b[3] = {64, BK, 2};
+    const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.d, BF, 3, t->d, d, st, b);
   }
   {  // C exchange scratch: regions [rings*G*slots][256 rows][nb] as {64, regions*256, nb/64}
@@ -604,7 +602,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     const uint64_t rows = kRagged ? mpad : (uint64_t)cfg->rings * cfg->ring * pair_c_slots(cfg) * 256;
     const uint64_t cols = kRagged ? N : (uint64_t)C::kN0;
     const uint64_t d[3] = {64, l2x ? rows : M, l2x ? cols / 64 : K / 64}, st[2] = {(l2x ? cols : K) * 2, 128};
-    const uint32_t b[3] = {64, 128, BK / 64};
+    const uint32_t b[3] = {64, 128, 2};
     ok = ok && make_map_nd(&maps.c, BF, 3, l2x ? (const void*)(wsb + wl.c_off) : t->a, d, st, b);
   }
   {  // E [M][L] bf16, box {64, 128}
@@ -692,7 +690,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.defer = cfg->ring - 1;
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
   a.finish_tma = pair_finish_regions(ch, cfg, rings);
-  a.prefetch = 256 / C::BK;  // 256 k ahead, measured on a cold L2 (profiles/r01/cold_prefetch.log)
+  a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
   // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
   // FF_VARIANT_NO_KROT restores the common order
   a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;

@@ -41,19 +41,13 @@ struct PairMaps {
   CUtensorMap slab; // split-N exchange regions 3D {32, 16, tiles*S*64} fp32, box {32, 128/S/8, 64} (no swizzle)
 };
 
-// k depth of one pipeline stage: 128 (3 x 64 KB stages) or 64 (6 x 32 KB stages: half the
-// bytes per stage, twice the lookahead in stages) -- an A/B build switch
-#ifndef FF_PAIR_BK
-#define FF_PAIR_BK 128
-#endif
 template <bool kGated, int kLB, int kStages>
 struct PairCfg {
   static constexpr int BM = 128;                  // rows per CTA (256 per pair)
-  static constexpr int BK = FF_PAIR_BK;           // k depth of one stage
-  static_assert(BK == 64 || BK == 128, "stage depth");
+  static constexpr int BK = 128;                  // k depth of one stage
   static constexpr int kN0 = kGated ? 128 : 256;  // C columns per pair per n-step
   static constexpr int kCW = kN0;
-  static constexpr int kSLOT = BM * BK * 2;       // one operand tile (A or B / C or D) per stage
+  static constexpr int kSLOT = 32768;             // one operand tile (A or B / C or D) per stage
   static constexpr int kSTAGE = 2 * kSLOT;
   static constexpr int kCHUNK_BYTES = BM * kCW * 2;  // own C chunk (bf16, K-major SW128 64-col tiles)
   // The own slot (32 KB) stages the drained C chunk for its TMA store (in
@@ -229,8 +223,7 @@ __global__ void __launch_bounds__(256, 1)
   auto done_flag = [&](int member) { return args.flags + (3u << 16) + ring * G + member; };
   // A tile: two K-major [128 x 64] SW128 tiles; B tile: MN-major [128 k x 64] tiles 16 KB apart
   auto a_desc = [](uint32_t slot, int kk) { return desc_kmajor_sw128(slot + (kk >> 2) * 16384 + (kk & 3) * 32); };
-  // MN-major B / D: [64-column block][BK k rows][128 B], blocks BK * 128 bytes apart
-  auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, C::BK * 128); };
+  auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
   constexpr int kChunks = kLB / 4;  // 16-byte column chunks per E row
 
   if (warp == 0) {
@@ -426,7 +419,7 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_full1, mbar_wait(full_bar(stage), phase));
           tc_fence_after();
           const uint32_t sb = base + stage * C::kSTAGE;
-          const uint32_t aslot = (C::kOwnFull && h == 0) ? own_slot + kb2 * (C::BK / 64) * 16384 : sb;
+          const uint32_t aslot = (C::kOwnFull && h == 0) ? own_slot + kb2 * 2 * 16384 : sb;
 #pragma unroll
           for (int kk = 0; kk < C::BK / 16; ++kk) {
             umma_bf16_pair(tmem_base + e_col, a_desc(aslot, kk), b_desc(sb + C::kSLOT, kk), idesc1,
