@@ -264,7 +264,11 @@ __global__ void __launch_bounds__(256, 1)
           const bool mine = !kQuad || ((seq++ & 1u) == pq);  // this pair issues the shared weight tile
           // L2 prefetch of the B tile `prefetch` k-blocks ahead: the weights
           // stream from HBM; the extra lead hides its latency behind 3 stages
+#ifdef FF_AB_NO_PREFETCH  // A/B builds only: without the L2 prefetches of weight tiles
+          const int pf = 0;
+#else
           const int pf = args.prefetch;
+#endif
           if (pf && kbl + pf < kblocks && (!kQuad || pq == 0)) {
             const int kbp = (kbl + pf + krot) % kblocks;
             if (!kGated || !kPackedB)
@@ -303,7 +307,11 @@ __global__ void __launch_bounds__(256, 1)
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
         if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
         if (!has_chunk(T, origin)) return;  // ragged n-step: no chunk from this origin
+#ifdef FF_AB_NO_FLAG_WAIT  // A/B builds only: cost of the ready-flag polls (results are not valid)
+        if (false) {
+#else
         if (from_l2 && !((ready >> origin) & 1ull)) {
+#endif
           // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
           FF_TIMED(w_flag, do {
@@ -808,27 +816,51 @@ __global__ void __launch_bounds__(256, 1)
     // A thread takes the two fp32 column chunks 2cp, 2cp+1 of one row: their bf16 result is
     // one 16-byte SW128 chunk, so 8 consecutive rows fill all 32 banks (one wavefront).
     const int rs = 31 - __clz(R);
-    const int n_pairs = n_items / 2;
+    const int per = (n_items / 2) >> 8;  // pair-items per thread (n_items / 2 is a multiple of 256)
+    // batches of 4 pair-items with every partial load of a split in flight together (one
+    // item at a time left each thread waiting out the shared-memory latency: ~1.7 us)
+    constexpr int kB = 4;
+    const uint32_t slot_bytes = (uint32_t)(R * kChunks * 16);
 #pragma unroll 1
-    for (int p0 = tid; p0 < n_pairs; p0 += 512) {
+    for (int b0 = 0; b0 < per; b0 += kB) {
+      float4 a[kB][2];
+      int off[kB];
 #pragma unroll
-      for (int q2 = 0; q2 < 2; ++q2) {
-        const int pi = p0 + 256 * q2;
-        if (pi >= n_pairs) break;  // warp-uniform (n_pairs is a multiple of 256)
-        const int cp = pi >> rs, rr = pi & (R - 1);
-        const int it0 = (2 * cp) * R + rr, it1 = it0 + R;  // items (chunk 2cp, row rr), (2cp+1, rr)
-        float4 a0 = *reinterpret_cast<const float4*>(src + it0 * 16);
-        float4 a1 = *reinterpret_cast<const float4*>(src + it1 * 16);
-#pragma unroll 1
-        for (int j = 1; j < S; ++j) {  // splits in order
-          const float4 f0 = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + it0 * 16);
-          const float4 f1 = *reinterpret_cast<const float4*>(src + j * (R * kChunks * 16) + it1 * 16);
-          a0.x += f0.x; a0.y += f0.y; a0.z += f0.z; a0.w += f0.w;
-          a1.x += f1.x; a1.y += f1.y; a1.z += f1.z; a1.w += f1.w;
+      for (int i = 0; i < kB; ++i) {
+        const int pi = tid + 256 * (b0 + i);
+        off[i] = ((2 * (pi >> rs)) * R + (pi & (R - 1))) * 16;  // item (chunk 2cp, row rr); +R*16: 2cp+1
+        if (b0 + i < per) {  // warp-uniform
+          a[i][0] = *reinterpret_cast<const float4*>(src + off[i]);
+          a[i][1] = *reinterpret_cast<const float4*>(src + off[i] + R * 16);
         }
+      }
+#pragma unroll 1
+      for (int j = 1; j < S; ++j) {  // splits in order
+        float4 f[kB][2];
+#pragma unroll
+        for (int i = 0; i < kB; ++i)
+          if (b0 + i < per) {
+            f[i][0] = *reinterpret_cast<const float4*>(src + j * slot_bytes + off[i]);
+            f[i][1] = *reinterpret_cast<const float4*>(src + j * slot_bytes + off[i] + R * 16);
+          }
+#pragma unroll
+        for (int i = 0; i < kB; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            a[i][h].x += f[i][h].x;
+            a[i][h].y += f[i][h].y;
+            a[i][h].z += f[i][h].z;
+            a[i][h].w += f[i][h].w;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        if (b0 + i >= per) break;
+        const int pi = tid + 256 * (b0 + i);
+        const int cp = pi >> rs, rr = pi & (R - 1);
         st_shared_v4(ebuf + (cp / 8) * (R * 128) + rr * 128 + (((cp % 8) ^ (rr & 7)) << 4),
-                     pack2(args.f16, a0.x, a0.y), pack2(args.f16, a0.z, a0.w), pack2(args.f16, a1.x, a1.y),
-                     pack2(args.f16, a1.z, a1.w));
+                     pack2(args.f16, a[i][0].x, a[i][0].y), pack2(args.f16, a[i][0].z, a[i][0].w),
+                     pack2(args.f16, a[i][1].x, a[i][1].y), pack2(args.f16, a[i][1].z, a[i][1].w));
       }
     }
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 22] = globaltimer_ns();

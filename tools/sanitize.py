@@ -26,6 +26,10 @@ CASES = [  # (kind, m, n, k, l, explicit CTA-pair config or None = auto lowering
     ("standard_ffn", 512, 2048, 512, 512, dict(ring=2, n_splits=4, nb=256, lb=256, exchange=2)),
     ("gated_ffn", 512, 2048, 512, 512, dict(ring=2, n_splits=8, nb=128, lb=256, exchange=2)),
     ("standard_ffn", 2048, 2048, 256, 512, dict(ring=2, n_splits=1, nb=256, lb=256, exchange=2)),
+    # DSM reduce-scatter of the split-N partials (FF_XCHG_L2_DSMR): split clusters of 2 / 4 / 8
+    ("standard_ffn", 256, 2048, 256, 512, dict(ring=2, n_splits=4, nb=128, lb=256, exchange=3)),
+    ("gated_ffn", 256, 1024, 256, 512, dict(ring=2, n_splits=8, nb=64, lb=256, exchange=3)),
+    ("standard_ffn", 200, 1024, 256, 256, dict(ring=1, n_splits=2, nb=128, lb=256, exchange=3)),
 ]
 
 
@@ -38,7 +42,10 @@ def main():
         host = {a: oracle.round_bf16(v) for a, v in oracle.make_inputs(kind, m, n, k, l, seed=11).items()}
         dev = {a: torch.from_numpy(v).cuda().to(torch.bfloat16) for a, v in host.items()}
         ref = oracle.dense_chain(kind, graph.activation, host, bf16_intermediate=True)
-        runs = (("pair", 2), ("pair", 4)) if fixed else (("dsm", 0), ("l2", 0), ("pair", 2), ("pair", 4))
+        if fixed:
+            runs = (("pair", 2), ("pair", 4)) if fixed["exchange"] == 2 else (("l2dsm", 0),)
+        else:
+            runs = (("dsm", 0), ("l2", 0), ("pair", 2), ("pair", 4))
         for exchange, variant in runs:
             lib.ff_set_variant(variant)
             try:

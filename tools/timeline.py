@@ -26,7 +26,9 @@ COUNTERS = ['prod_total', 'prod_w_empty', 'prod_w_flag', 'mma_total', 'mma_w_ful
             'epi_store', 'epi_E']
 SHAPES = {"llama": (512, 8192, 2048, 2048, 2, True), "gpt67b": (512, 16384, 4096, 4096, 1, False),
           "opt": (4096, 8192, 2048, 2048, 1, False), "gpt2s": (512, 3072, 768, 768, 3, False),
-          "opt32k": (32768, 8192, 2048, 2048, 1, False)}
+          "opt32k": (32768, 8192, 2048, 2048, 1, False),
+          # phase probes: GEMM0-dominated (one ring member, L = 256) and hop-dominated (K = 128)
+          "g0only": (32768, 8192, 4096, 256, 1, False), "hopsonly": (32768, 8192, 128, 2048, 1, False)}
 
 
 def setup(m, n, k, l, act, gated, xchg, lib):
