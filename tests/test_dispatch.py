@@ -14,7 +14,7 @@ def test_shipped_tables_cover_the_baseline_families():
         assert (t.kind, t.activation, t.n, t.k, t.l) == (kind, act, n, k, l)
         assert t.bins == sorted(t.bins) and len(t.configs) == len(t.bins)
         for c in t.configs:
-            assert c["exchange"] in (0, 1, 2) and c["ring"] >= 1 and c["n_splits"] >= 1 and c["ms"] > 0
+            assert c["exchange"] in (0, 1, 2, 3) and c["ring"] >= 1 and c["n_splits"] >= 1 and c["ms"] > 0
 
 
 def test_bin_lookup_and_round_trip(tmp_path):
