@@ -194,6 +194,7 @@ void ff_set_profile_buffer(void* dev_ptr);
 #define FF_VARIANT_WEIGHTS_EVICT_LAST 0x40u  /* pair kernel: weight tiles + prefetches with L2 evict_last */
 #define FF_VARIANT_NO_DISCARD 0x80u          /* pair kernel: keep dead exchange scratch in L2 (no discard) */
 #define FF_VARIANT_SCRATCH_DISCARD 0x100u    /* pair kernel: also discard the C exchange scratch at exit */
+#define FF_VARIANT_NO_SERP 0x200u            /* pair kernel: every unit walks its n-steps in order */
 void ff_set_variant(uint32_t flags);
 
 /* Thread-local message for the last non-OK status. */

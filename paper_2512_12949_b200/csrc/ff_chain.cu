@@ -710,6 +710,10 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // at exit (FF_VARIANT_SCRATCH_DISCARD) moves no further bytes and costs 1-2 us
   a.discard = (g_variant & FF_VARIANT_NO_DISCARD) ? 0 : (g_variant & FF_VARIANT_SCRATCH_DISCARD) ? 3 : 1;
   a.cscratch = reinterpret_cast<__nv_bfloat16*>(wsb + wl.c_off);
+  // rings that run several units: odd units walk their n-steps backwards so they start on
+  // the weights the previous unit read last (OPT M=4096: second wave of units re-read the
+  // weights from DRAM; FF_VARIANT_NO_SERP restores the common order)
+  a.serp = (!kRagged && rings < cfg->units && !(g_variant & FF_VARIANT_NO_SERP)) ? 1 : 0;
   if (wl.e_memset) {
     cudaError_t e0 = cudaMemsetAsync(wsb + wl.e_off, 0, (size_t)M * L * sizeof(float), stream);
     if (e0 != cudaSuccess) return fail(FF_ERR_CUDA, std::string("memset: ") + cudaGetErrorString(e0));

@@ -77,6 +77,8 @@ struct ChainArgs {
   int cpolicy;         // pair kernel: L2 hint for the C exchange scratch (stores and loads)
   int split_cl;        // L2 kernels: the S N splits of an E tile are one thread-block cluster and combine
                        // their fp32 partials by a DSM reduce-scatter (FF_XCHG_L2_DSMR)
+  int serp;            // pair kernel: a ring's odd units run their n-steps in reverse order, so the
+                       // weights the previous unit read last (still in L2) are read first
   int discard;         // pair kernel: drop dead scratch from L2 without a DRAM write-back once its last
                        // reader is done: bit 0 the split-N exchange regions, bit 1 the C scratch
   __nv_bfloat16* cscratch;  // pair kernel: C exchange scratch base (row-major [regions * 256][kN0])

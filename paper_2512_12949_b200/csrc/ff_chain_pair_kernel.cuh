@@ -124,6 +124,13 @@ __global__ void __launch_bounds__(256, 1)
   // chunk t * G + origin of a split is GEMM0'd by member `origin` in n-step t.  A member
   // without a chunk keeps every barrier handshake (empty GEMM0 commits, drain-less
   // arrivals) and skips the work.  T is the member's global step index.
+  // physical n-step (column position) of global step T: a ring's odd units walk their
+  // n-steps backwards (serpentine), so the first weights they read are the ones the
+  // previous unit read last.  Flags, scratch slots and the schedule keep the logical step.
+  auto nstep = [&](int T) {
+    const int t = T % steps;
+    return (!kRagged && args.serp && ((T / steps) & 1)) ? steps - 1 - t : t;
+  };
   auto has_chunk = [&](int T, int origin) {
     if (!kRagged) return true;
     const int split = unit_of(T / steps).split;
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(256, 1)
         if (kb0 >= kb1 || !has_chunk(T, p)) return;
         const Unit u = unit_of(T / steps);
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
-        const int nblk = (u.n0 + ((T % steps) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
+        const int nblk = (u.n0 + (nstep(T) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
         for (int kbl = kb0; kbl < kb1; ++kbl) {
           const int kb = (kbl + krot) % kblocks;  // physical k-block (members start at staggered k)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(256, 1)
         const Unit u = unit_of(T / steps);
         const int t = T % steps;
         const int origin = (p - h + G) % G;
-        const int ncol0 = u.n0 + (t * G + origin) * C::kN0;
+        const int ncol0 = u.n0 + (nstep(T) * G + origin) * C::kN0;
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
         if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(256, 1)
           fence_proxy_async_global();
         }
         if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
-          const int ncol_pf = u.n0 + (t * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
+          const int ncol_pf = u.n0 + (nstep(T) * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
             tma_prefetch_l2_3d_h(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk, pol_w);
         }
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(256, 1)
             st_shared_v4(swz(tile, ch + j), pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           const int grow = u.m0 + (int)q * C::BM + row;
           if (args.c_debug != nullptr && grow < args.M) {
-            const int ncol = u.n0 + (t * G + p) * C::kN0 + c0;
+            const int ncol = u.n0 + (nstep(T) * G + p) * C::kN0 + c0;
             uint4* dst = reinterpret_cast<uint4*>(args.c_debug + (size_t)grow * args.N + ncol);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);

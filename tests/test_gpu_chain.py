@@ -255,6 +255,29 @@ def test_pair_kernel_variants_match_oracle_and_repeat_bitwise(case, mode):
     assert torch.equal(out1, out2), "split-N reductions must be deterministic"
 
 
+# serpentine n-step order (odd units of a ring walk their n-steps backwards) against the
+# common order: both match the oracle (OPT M=4096: 16 units on 9 rings)
+@pytest.mark.parametrize("mode", [0x0, 0x200], ids=["serpentine", "no-serp"])
+def test_pair_kernel_serpentine_units_match_oracle(mode):
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = "standard_ffn", "relu", 4096, 8192, 2048, 2048
+    graph = _graph(kind, act, m, n, k, l)
+    host, dev = _inputs(kind, m, n, k, l, seed=13)
+    lib = nat.load()
+    lib.ff_set_variant(mode)
+    try:
+        cfg = runtime.lower(graph, None, 148, "pair")
+        assert cfg.units > cfg.rings
+        out = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+    finally:
+        lib.ff_set_variant(0)
+    _check(kind, act, host, out)
+
+
 def _random_cases(n, seed):
     rng = __import__("random").Random(seed)
     cases = []

@@ -1,8 +1,11 @@
-# scratch driver (r02 session 4i): A/B builds -- cost of the flag polls and of the weight L2 prefetches
+# scratch driver (r02 session 5c): serpentine unit order A/B (OPT M=4096 DRAM bytes, timelines)
 set -x
-O=gpurun_out/r02s4i; mkdir -p $O
-for lib in libff_chain libff_ab_noflag libff_ab_nopf; do
-  export FF_CHAIN_LIB=paper_2512_12949_b200/$lib.so
-  timeout 300 python tools/timeline.py gpt67b llama opt opt32k hopsonly counters > $O/timeline_$lib.log 2>&1
+O=gpurun_out/r02s5c; mkdir -p $O
+timeout 600 python -m pytest tests/test_gpu_chain.py -m gpu -x -q -k "serpentine or variants" > $O/tests.log 2>&1; echo "tests rc=$?"; tail -3 $O/tests.log
+for v in 0x0 0x200; do
+  timeout 300 ncu --cache-control none --clock-control none --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv --log-file $O/dram_opt4096_$v.csv python tools/dram_bytes.py run opt13b_m4096 fused variant=$v > /dev/null 2>&1
+  python tools/dram_bytes.py parse $O/dram_opt4096_$v.csv > $O/dram_opt4096_$v.json
+  cat $O/dram_opt4096_$v.json
+  timeout 300 python tools/timeline.py opt opt32k variant=$v > $O/timeline_$v.log 2>&1
+  grep "==" $O/timeline_$v.log
 done
-grep -h "events\|mma_total\|w_full\|prod_w_flag" $O/timeline_*.log
