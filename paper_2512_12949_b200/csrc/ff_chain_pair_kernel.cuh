@@ -751,36 +751,23 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();  // warps 0/1 arrive from divergent role loops; tcgen05.ld is warp-collective
     tc_fence_after();
     if (issuer) FF_STAMP(30);
-    // shared memory (drained stages): slot s = [kChunks][R rows][16 B] partial of split s
-    // for this split's rows (own partial staged from TMEM, partners' by TMA), then
-    // the bf16 E rows [kLB/64][R][128 B] (SW128) for one TMA store
+    // shared memory (drained stages): slot j != sp = [kChunks][R rows][16 B] partner j's
+    // partial of this split's rows (TMA), then the bf16 E rows [kLB/64][R][128 B] (SW128)
+    // for one TMA store.  The own partial of this split's rows stays in TMEM until the sum.
     const uint32_t slot0 = base;
     const uint32_t ebuf = base + S * R * kChunks * 16;
-    {
-      float* const dst = region(sp) + row * 4;
-      const uint32_t own = slot0 + sp * (R * kChunks * 16) + (row - sp * R) * 16;
-#pragma unroll 1
-      for (int c0 = c_lo; c0 < c_lo + kLB / 2; c0 += 64) {
-        float v[32], w[32];
-        tmem_ld32x2(lane_base + e_col + c0, lane_base + e_col + c0 + 32, v, w);
-        if (slice != sp) {  // another split's row: straight to this split's exchange region
+    // Every thread loads its row's half of the E partial (kLB/2 columns) from TMEM once,
+    // with a single wait: rows of another split's slice go straight to this split's
+    // exchange region, rows of this split's slice stay in registers for the sum.
+    constexpr int kHalf = kLB / 2;
+    float ev[kHalf];
+    tmem_ld32xn<kHalf / 32>(lane_base + e_col + c_lo, ev);
+    if (slice != sp) {
+      float* const dst = region(sp) + row * 4 + (size_t)(c_lo / 4) * 512;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            st_global_v4(dst + (size_t)(c0 / 4 + j) * 512, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
-                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
-            st_global_v4(dst + (size_t)(c0 / 4 + 8 + j) * 512, __float_as_uint(w[4 * j]),
-                         __float_as_uint(w[4 * j + 1]), __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
-          }
-        } else {  // own row: shared-memory slot sp
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            st_shared_v4(own + (c0 / 4 + j) * (R * 16), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
-                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
-            st_shared_v4(own + (c0 / 4 + 8 + j) * (R * 16), __float_as_uint(w[4 * j]), __float_as_uint(w[4 * j + 1]),
-                         __float_as_uint(w[4 * j + 2]), __float_as_uint(w[4 * j + 3]));
-          }
-        }
-      }
+      for (int k = 0; k < kHalf / 4; ++k)
+        st_global_v4(dst + (size_t)k * 512, __float_as_uint(ev[4 * k]), __float_as_uint(ev[4 * k + 1]),
+                     __float_as_uint(ev[4 * k + 2]), __float_as_uint(ev[4 * k + 3]));
     }
     // the barrier orders every thread's region stores before the issuer's
     // gpu-scope release (cumulative; the split-K semaphore pattern), no
@@ -806,68 +793,39 @@ __global__ void __launch_bounds__(256, 1)
     }
     mbar_wait(e_load, 0);
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
-    if (args.discard & 1) {  // the partners' rows of this slice are read exactly once: drop them from L2
-      const int lines = kChunks * R / 8;  // 128-byte lines of one (region, slice) block
-      for (int j = 0; j < S; ++j) {
-        if (j == sp) continue;
-        const uint8_t* blk = reinterpret_cast<const uint8_t*>(region(j)) + sp * R * 16;
-        for (int i = tid; i < lines; i += 256)
-          discard_l2_line(blk + (size_t)(i / (R / 8)) * 2048 + (i % (R / 8)) * 128);
-      }
-    }
-    // sum in split order (deterministic), cast, stage bf16; item = (chunk c, row rr)
-    const uint8_t* const src = smem_gen;
-    const int n_items = R * kChunks;
-    // R = 128 / S is a power of two (pair_finish_regions): item -> (chunk, row) by shifts (a
-    // runtime division per item made the sum ~3x slower than its shared-memory traffic).
-    // A thread takes the two fp32 column chunks 2cp, 2cp+1 of one row: their bf16 result is
-    // one 16-byte SW128 chunk, so 8 consecutive rows fill all 32 banks (one wavefront).
-    const int rs = 31 - __clz(R);
-    const int per = (n_items / 2) >> 8;  // pair-items per thread (n_items / 2 is a multiple of 256)
-    // batches of 4 pair-items with every partial load of a split in flight together (one
-    // item at a time left each thread waiting out the shared-memory latency: ~1.7 us)
-    constexpr int kB = 4;
-    const uint32_t slot_bytes = (uint32_t)(R * kChunks * 16);
-#pragma unroll 1
-    for (int b0 = 0; b0 < per; b0 += kB) {
-      float4 a[kB][2];
-      int off[kB];
+    // sum (deterministic order: own partial, then the partners in split order), cast,
+    // stage bf16.  The own partial is in registers; a warp's 32 rows of one 16-byte
+    // column chunk of a partner slot are 512 contiguous bytes, and the bf16 row stores
+    // are SW128 (8 rows cover all banks).
+    if (slice == sp) {
+      const int rr = row - sp * R;
+      const uint32_t part = slot0 + rr * 16 + (c_lo / 4) * (R * 16);
 #pragma unroll
-      for (int i = 0; i < kB; ++i) {
-        const int pi = tid + 256 * (b0 + i);
-        off[i] = ((2 * (pi >> rs)) * R + (pi & (R - 1))) * 16;  // item (chunk 2cp, row rr); +R*16: 2cp+1
-        if (b0 + i < per) {  // warp-uniform
-          a[i][0] = *reinterpret_cast<const float4*>(src + off[i]);
-          a[i][1] = *reinterpret_cast<const float4*>(src + off[i] + R * 16);
+      for (int k = 0; k < kHalf / 4; k += 8) {  // 32 columns per round
+#pragma unroll 1
+        for (int j = 0; j < S; ++j) {
+          if (j == sp) continue;
+          float4 f[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            f[i] = ld_shared_f4(part + j * (R * kChunks * 16) + (k + i) * (R * 16));
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            ev[4 * (k + i)] += f[i].x;
+            ev[4 * (k + i) + 1] += f[i].y;
+            ev[4 * (k + i) + 2] += f[i].z;
+            ev[4 * (k + i) + 3] += f[i].w;
+          }
         }
-      }
-#pragma unroll 1
-      for (int j = 1; j < S; ++j) {  // splits in order
-        float4 f[kB][2];
+        const int c0 = c_lo + 4 * k;  // first column of the round
+        const int ch = (c0 % 64) / 8;
+        const uint32_t dst = ebuf + (c0 / 64) * (R * 128) + rr * 128;
 #pragma unroll
-        for (int i = 0; i < kB; ++i)
-          if (b0 + i < per) {
-            f[i][0] = *reinterpret_cast<const float4*>(src + j * slot_bytes + off[i]);
-            f[i][1] = *reinterpret_cast<const float4*>(src + j * slot_bytes + off[i] + R * 16);
-          }
-#pragma unroll
-        for (int i = 0; i < kB; ++i)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            a[i][h].x += f[i][h].x;
-            a[i][h].y += f[i][h].y;
-            a[i][h].z += f[i][h].z;
-            a[i][h].w += f[i][h].w;
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < kB; ++i) {
-        if (b0 + i >= per) break;
-        const int pi = tid + 256 * (b0 + i);
-        const int cp = pi >> rs, rr = pi & (R - 1);
-        st_shared_v4(ebuf + (cp / 8) * (R * 128) + rr * 128 + (((cp % 8) ^ (rr & 7)) << 4),
-                     pack2(args.f16, a[i][0].x, a[i][0].y), pack2(args.f16, a[i][0].z, a[i][0].w),
-                     pack2(args.f16, a[i][1].x, a[i][1].y), pack2(args.f16, a[i][1].z, a[i][1].w));
+        for (int i = 0; i < 4; ++i)
+          st_shared_v4(dst + (((ch + i) ^ (rr & 7)) << 4), pack2(args.f16, ev[4 * k + 8 * i], ev[4 * k + 8 * i + 1]),
+                       pack2(args.f16, ev[4 * k + 8 * i + 2], ev[4 * k + 8 * i + 3]),
+                       pack2(args.f16, ev[4 * k + 8 * i + 4], ev[4 * k + 8 * i + 5]),
+                       pack2(args.f16, ev[4 * k + 8 * i + 6], ev[4 * k + 8 * i + 7]));
       }
     }
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 22] = globaltimer_ns();
@@ -878,6 +836,16 @@ __global__ void __launch_bounds__(256, 1)
       bulk_commit();
       FF_STAMP(26);
       bulk_wait_read0();
+    }
+    // (off the critical path: after the sum, the discards no longer delay its loads)
+    if (args.discard & 1) {  // the partners' rows of this slice are read exactly once: drop them from L2
+      const int lines = kChunks * R / 8;  // 128-byte lines of one (region, slice) block
+      for (int j = 0; j < S; ++j) {
+        if (j == sp) continue;
+        const uint8_t* blk = reinterpret_cast<const uint8_t*>(region(j)) + sp * R * 16;
+        for (int i = tid; i < lines; i += 256)
+          discard_l2_line(blk + (size_t)(i / (R / 8)) * 2048 + (i % (R / 8)) * 128);
+      }
     }
   }
 

@@ -533,6 +533,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 x kN consecutive TMEM columns of this warp's lane quarter into registers (kN x
+// 32x32b.x32 loads behind one tcgen05.wait::ld; the registers are threaded through the
+// wait, 64 per asm statement, so no consumer is scheduled before it).
+template <int kN>
+__device__ __forceinline__ void tmem_ld32xn(uint32_t taddr, float (&v)[32 * kN]) {
+  uint32_t r[32 * kN];
+#pragma unroll
+  for (int g = 0; g < kN; ++g)
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[32 * g + 0]), "=r"(r[32 * g + 1]), "=r"(r[32 * g + 2]), "=r"(r[32 * g + 3]), "=r"(r[32 * g + 4]),
+          "=r"(r[32 * g + 5]), "=r"(r[32 * g + 6]), "=r"(r[32 * g + 7]), "=r"(r[32 * g + 8]), "=r"(r[32 * g + 9]),
+          "=r"(r[32 * g + 10]), "=r"(r[32 * g + 11]), "=r"(r[32 * g + 12]), "=r"(r[32 * g + 13]),
+          "=r"(r[32 * g + 14]), "=r"(r[32 * g + 15]), "=r"(r[32 * g + 16]), "=r"(r[32 * g + 17]),
+          "=r"(r[32 * g + 18]), "=r"(r[32 * g + 19]), "=r"(r[32 * g + 20]), "=r"(r[32 * g + 21]),
+          "=r"(r[32 * g + 22]), "=r"(r[32 * g + 23]), "=r"(r[32 * g + 24]), "=r"(r[32 * g + 25]),
+          "=r"(r[32 * g + 26]), "=r"(r[32 * g + 27]), "=r"(r[32 * g + 28]), "=r"(r[32 * g + 29]),
+          "=r"(r[32 * g + 30]), "=r"(r[32 * g + 31])
+        : "r"(taddr + 32u * g));
+#define FF_TIE8(o) "+r"(r[o]), "+r"(r[o + 1]), "+r"(r[o + 2]), "+r"(r[o + 3]), "+r"(r[o + 4]), "+r"(r[o + 5]), \
+                   "+r"(r[o + 6]), "+r"(r[o + 7])
+#pragma unroll
+  for (int g = 0; g < kN; g += 2) {  // (the first wait completes every load; later ones only tie registers)
+    if (g + 1 < kN)
+      asm volatile("tcgen05.wait::ld.sync.aligned;"
+                   : FF_TIE8(32 * g), FF_TIE8(32 * g + 8), FF_TIE8(32 * g + 16), FF_TIE8(32 * g + 24),
+                     FF_TIE8(32 * g + 32), FF_TIE8(32 * g + 40), FF_TIE8(32 * g + 48), FF_TIE8(32 * g + 56)::"memory");
+    else
+      asm volatile("tcgen05.wait::ld.sync.aligned;"
+                   : FF_TIE8(32 * g), FF_TIE8(32 * g + 8), FF_TIE8(32 * g + 16), FF_TIE8(32 * g + 24)::"memory");
+  }
+#undef FF_TIE8
+#pragma unroll
+  for (int i = 0; i < 32 * kN; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // Two 32-column TMEM loads (e.g. the gate and up accumulators of a SwiGLU
 // chunk) behind a single tcgen05.wait::ld; the registers are threaded through
 // the wait so no consumer can be scheduled before it.

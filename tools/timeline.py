@@ -52,7 +52,8 @@ def setup(m, n, k, l, act, gated, xchg, lib):
 
 def main(argv):
     lib = nat.load()
-    flush_buf = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
+    flush_buf = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
+    sink = torch.empty((), dtype=torch.float32, device='cuda')
     sel = [a for a in argv if a in SHAPES] or ["gpt67b", "llama"]
     variant = next((int(a.split("=")[1], 0) for a in argv if a.startswith("variant=")), 0)
     lib.ff_set_variant(variant)
@@ -69,7 +70,9 @@ def main(argv):
             f()
         runs = []
         for _ in range(5):
-            if 'warm' not in argv:
+            if 'rflush' in argv:  # read-only flush: leaves clean lines (no dirty evictions afterwards)
+                torch.sum(flush_buf, dim=0, out=sink)
+            elif 'warm' not in argv:
                 flush_buf.add_(1.0)
             ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             buf.zero_()
@@ -94,6 +97,13 @@ def main(argv):
             if col.numel():
                 print(f"   {NAMES[i]:11s} min {col.min().item():7.1f} mean {col.mean().item():7.1f} "
                       f"max {col.max().item():7.1f} us")
+        if 'res' in argv:  # globaltimer resolution: distinct raw values of the entry and exit stamps
+            for i in (0, 10, 15):
+                raw = v[:, i][v[:, i] > 0].long()
+                u = torch.unique(raw)
+                d = (u[1:] - u[:-1]) if u.numel() > 1 else u
+                print(f"   stamp {NAMES[i]}: {u.numel()} distinct of {raw.numel()}, min step {int(d.min())} ns, "
+                      f"values mod 1000: {sorted(set((raw % 1000).tolist()))[:8]}")
         if 'counters' in argv:  # per-role wait counters (clock64 cycles, FF_TIMED): mean / max over CTAs
             live = cnt[valid]
             for i, nm in enumerate(COUNTERS):
