@@ -704,6 +704,7 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
               : (g_variant & FF_VARIANT_WEIGHTS_EVICT_LAST) ? ff::L2_EVICT_LAST
                                                             : ff::L2_NORMAL;
   a.cpolicy = (g_variant & FF_VARIANT_SCRATCH_NORMAL) ? ff::L2_NORMAL : ff::L2_EVICT_LAST;
+  a.epolicy = (g_variant & FF_VARIANT_E_EVICT_FIRST) ? ff::L2_EVICT_FIRST : ff::L2_NORMAL;
   // dead split-N exchange regions leave L2 without a DRAM write-back (FF_VARIANT_NO_DISCARD: keep
   // them).  Measured (profiles/r02/discard_ab.md): GPT-6.7B DRAM 286.0 -> 277.8 MB (1.004x the
   // algorithmic bytes), LLaMA-1B 118.2 -> 105.9 MB, no time cost; also discarding the C scratch

@@ -75,6 +75,7 @@ struct ChainArgs {
   int c_slots;         // pair kernel: C exchange slots per ring member (scratch reused every c_slots n-steps)
   int wpolicy;         // pair kernel: L2 hint (L2Hint) for weight tiles and their L2 prefetches
   int cpolicy;         // pair kernel: L2 hint for the C exchange scratch (stores and loads)
+  int epolicy;         // pair kernel: L2 hint for the E tile stores (E is never re-read by the kernel)
   int split_cl;        // L2 kernels: the S N splits of an E tile are one thread-block cluster and combine
                        // their fp32 partials by a DSM reduce-scatter (FF_XCHG_L2_DSMR)
   int serp;            // pair kernel: a ring's odd units run their n-steps in reverse order, so the

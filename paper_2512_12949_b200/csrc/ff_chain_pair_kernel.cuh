@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(256, 1)
     // row r of a 128-byte-row SW128 tile: 16-byte chunk c lives at chunk c ^ (r & 7)
     auto swz = [&](uint32_t tile, int ch) { return tile + row * 128 + ((ch ^ (row & 7)) << 4); };
     const uint64_t pol_c = l2_policy(args.cpolicy);  // C exchange scratch
+    const uint64_t pol_e = l2_policy(args.epolicy);  // E tiles
     // before chunk T overwrites slot T % c_slots: every ring member's flag of step
     // T - c_slots + 2, i.e. all of them have read step T - c_slots (see c_row)
     auto wait_slot_free = [&](int T) {
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(256, 1)
           named_bar_sync(1, 128);
           if (issuer) {
             if (bf16_out)
-              tma_store_3d(&maps.e3, base, 0, erow, u.l0 / 64);
+              tma_store_3d_h(&maps.e3, base, 0, erow, u.l0 / 64, l2_policy(args.epolicy));
             else
               tma_reduce_add_3d(&maps.w3, base, 0, erow, u.l0 / 32);
             bulk_commit();
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int c0 = g0; c0 < g1; c0 += cols_per_tile) {
               const uint32_t tile = stg + ((c0 - g0) / cols_per_tile) * 16384;
               if (bf16_out)
-                tma_store_2d(&maps.e, tile, u.l0 + c0, erow);
+                tma_store_2d_h(&maps.e, tile, u.l0 + c0, erow, pol_e);
               else
                 tma_reduce_add_2d(&maps.w, tile, u.l0 + c0, erow);
             }
@@ -832,7 +833,7 @@ __global__ void __launch_bounds__(256, 1)
     fence_proxy_async_smem();
     __syncthreads();
     if (issuer) {
-      tma_store_3d(&maps.er, ebuf, 0, erow + sp * R, u.l0 / 64);
+      tma_store_3d_h(&maps.er, ebuf, 0, erow + sp * R, u.l0 / 64, l2_policy(args.epolicy));
       bulk_commit();
       FF_STAMP(26);
       bulk_wait_read0();

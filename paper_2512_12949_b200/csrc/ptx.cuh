@@ -398,6 +398,12 @@ __device__ __forceinline__ void tma_load_4d_pair_mcast_h(uint32_t dst, const voi
       "l"(desc), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar), "h"(mask), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d_h(const void* desc, uint32_t src, int32_t c0, int32_t c1, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                   desc),
+               "r"(src), "r"(c0), "r"(c1), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_3d_h(const void* desc, uint32_t src, int32_t c0, int32_t c1, int32_t c2,
                                                uint64_t pol) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
