@@ -763,7 +763,10 @@ __global__ void __launch_bounds__(256, 1)
     constexpr int kHalf = kLB / 2;
     float ev[kHalf];
     tmem_ld32xn<kHalf / 32>(lane_base + e_col + c_lo, ev);
-    if (slice != sp) {
+#ifndef FF_AB_TAIL  // A/B builds only (results invalid): 1 no region stores, 2 + no partner wait/load, 3 no sum
+#define FF_AB_TAIL 0
+#endif
+    if (slice != sp && FF_AB_TAIL != 1 && FF_AB_TAIL != 2) {
       float* const dst = region(sp) + row * 4 + (size_t)(c_lo / 4) * 512;
 #pragma unroll
       for (int k = 0; k < kHalf / 4; ++k)
@@ -779,7 +782,7 @@ __global__ void __launch_bounds__(256, 1)
       st_release_gpu_u32(slab_flag(sp), epoch);
       if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 25] = globaltimer_ns();
       uint32_t polls = 0;
-      for (int j = 0; j < S; ++j) {
+      for (int j = 0; j < S && FF_AB_TAIL != 2; ++j) {
         if (j == sp) continue;
         while (ld_relaxed_gpu_u32(slab_flag(j)) != epoch)
           if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
@@ -787,12 +790,14 @@ __global__ void __launch_bounds__(256, 1)
       fence_acq_rel_gpu();
       fence_proxy_async_global();
       if (args.prof) args.prof[vcta * FF_PROF_STRIDE + 27] = globaltimer_ns();
-      mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kChunks * 16));
-      for (int j = 0; j < S; ++j)
-        if (j != sp)
-          tma_load_3d(slot0 + j * (R * kChunks * 16), &maps.slab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
+      if (FF_AB_TAIL != 2) {
+        mbar_expect_tx(e_load, (uint32_t)((S - 1) * R * kChunks * 16));
+        for (int j = 0; j < S; ++j)
+          if (j != sp)
+            tma_load_3d(slot0 + j * (R * kChunks * 16), &maps.slab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
+      }
     }
-    mbar_wait(e_load, 0);
+    if (FF_AB_TAIL != 2) mbar_wait(e_load, 0);
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
     // sum (deterministic order: own partial, then the partners in split order), cast,
     // stage bf16.  The own partial is in registers; a warp's 32 rows of one 16-byte
@@ -804,7 +809,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int k = 0; k < kHalf / 4; k += 8) {  // 32 columns per round
 #pragma unroll 1
-        for (int j = 0; j < S; ++j) {
+        for (int j = 0; j < S && FF_AB_TAIL != 3; ++j) {
           if (j == sp) continue;
           float4 f[8];
 #pragma unroll
