@@ -748,12 +748,15 @@ bool quad_ok(const ffKernelConfig* cfg, bool gated) {
   int rings = std::min(pair_rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring)) & ~1;
   if (rings < 2) return false;
   if (g_variant & FF_VARIANT_FORCE_QUAD) return true;  // A/B and tests: quad whenever it can launch
+  // one-wave standard FFN (GPT-6.7B): plain pairs -- interleaved A/B over 600 steps each, both orders
+  // (profiles/r02/s5/ab_quad_long.log): -1.0 / -1.2 %; the quad halves the L2 reads of the weights but the
+  // main loop is bound by per-SM operand ingest, not by L2.  Gated FFN (LLaMA-1B: +2.6 % without) and
+  // multi-unit rings keep quads: OPT M=4096 is 0.8 % faster on 9 plain rings but moves 171.6 instead of
+  // 161.7 MB of DRAM (9 rings of C scratch, a 9 + 7 second wave; r02s5v vs r02s5o)
+  if (!gated && cfg->units <= pair_rings) return false;
   // quads need an even ring count: when that costs a wave of units (OPT M=32768: 128 units
   // on 8 quad rings = 16 waves vs 9 pair rings = 15), plain pairs win (-2.4 %, A/B)
   const int waves_quad = (cfg->units + rings - 1) / rings, waves_pair = (cfg->units + pair_rings - 1) / pair_rings;
-  // (gated one-wave chains: plain pairs 0.35 us faster than quads on one box, 0.08 us slower
-  // on another -- no rule; quads stay the default)
-  (void)gated;
   return waves_quad <= waves_pair;
 }
 
