@@ -911,6 +911,17 @@ const char* ff_last_error(void) { return g_last_error.c_str(); }
 // (unsigned long long[grid_ctas][16]) into this device buffer.
 void ff_set_profile_buffer(void* dev_ptr) { g_prof = reinterpret_cast<unsigned long long*>(dev_ptr); }
 void ff_set_variant(uint32_t flags) { g_variant = flags; }
+
+#ifdef FF_DIAG_WATCHDOG
+// Diagnostic builds only: out[0] = waits expired since the last call, out[1 + 2i] = source line << 40 |
+// block << 20 | thread and out[2 + 2i] = wait-specific info of the first 512; then cleared.
+int ff_diag_read(unsigned long long* out) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, ff::ff_diag, sizeof(ff::ff_diag));
+  static const unsigned long long z[1 + 2 * 512] = {};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(ff::ff_diag, z, sizeof(z));
+  return e == cudaSuccess ? FF_OK : FF_ERR_CUDA;
+}
+#endif
 const char* ff_version(void) { return "ff_chain 0.1.0 sm_100a"; }
 
 int ff_auto_config_ex(const ffChainDesc* ch, int32_t num_sms, int32_t exchange, ffKernelConfig* out) {

@@ -203,7 +203,7 @@ __device__ __forceinline__ void split_finish(const ChainArgs& args, uint32_t* co
     if (shared) {
       uint32_t polls = 0;
       while (ld_acquire_gpu_u32(counter) < S)
-        if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+        if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(ld_acquire_gpu_u32(counter));
     }
     st_shared_u32(bcast, ticket);
   }
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t* f = args.flags + tile;  // unit id == m tile (ring 1, one step, one l cluster)
             uint32_t polls = 0;
             FF_TIMED(w_flag, while (ld_acquire_gpu_u32(f) != epoch) {
-              if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+              if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)ld_acquire_gpu_u32(f) << 32) | epoch);
             });
           }
           fence_proxy_async_global();
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t* f = flag_addr(u, t, origin);
           uint32_t polls = 0;
           FF_TIMED(w_flag, while (ld_acquire_gpu_u32(f) != epoch) {
-            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+            if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)ld_acquire_gpu_u32(f) << 32) | epoch);
           });
           fence_proxy_async_global();
         }
@@ -493,6 +493,9 @@ __global__ void __launch_bounds__(256, 1)
         pr[2] = w_flag;
       }
     }
+    // The other 31 lanes wait here, not in a spin loop of their own: two divergent spin-wait
+    // paths in one warp can starve the role lane (found on hardware in the pair kernel).
+    __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (elect_one()) {
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(256, 1)
         pr[8] = w_eempty;
       }
     }
+    __syncwarp();  // see warp 0
   } else if (warp == 2) {
     // ===== DSM shuffle, send side: direct pushes of the own chunk (kMode 0) =====
     // At hop h ring member q consumes the chunk of origin (q-h) mod G, so
@@ -628,6 +632,7 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(own_free);
       }
     }
+    __syncwarp();  // see warp 0
   } else if (warp == 3) {
     // ===== DSM shuffle, receive side: ack landing, recycle, credit (kMode 0) =====
     if (kDSM && G > 1 && elect_one()) {
@@ -646,6 +651,7 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+    __syncwarp();  // see warp 0
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;  // TMEM lane quadrant
@@ -707,6 +713,7 @@ __global__ void __launch_bounds__(256, 1)
           st_release_gpu_u32(flag_addr(u, t, (int)p), epoch);
           mbar_arrive(own_free);
         }
+        __syncwarp();  // lanes 1-31 must not spin on the next barrier while the issuer publishes
       }
       if (t == steps - 1) {
         // E tile of this unit: TMEM -> registers -> global
@@ -782,7 +789,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < S; ++j) {
               if (j == sp) continue;
               while (ld_relaxed_gpu_u32(flags + j) != epoch)
-                if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+                if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)ld_relaxed_gpu_u32(flags + j) << 32) | epoch);
             }
             fence_acq_rel_gpu();
             fence_proxy_async_global();
@@ -792,6 +799,7 @@ __global__ void __launch_bounds__(256, 1)
               if (j != sp)
                 tma_load_3d(base + j * (R * kChunks * 16), &tmSlab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
           }
+          __syncwarp();  // the issuer's lanes wait for it here, not spinning on own_free / e_load
           mbar_wait(own_free, T & 1);  // the own slot stages the bf16 rows (DSM pushes read it until acked)
           mbar_wait(e_load, 0);
           // sum in split order, cast, stage [kLB/64][R][128 B] SW128 for one TMA store

@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(256, 1)
               for (int j = 0; j < 8; ++j)
                 if (v[j] == epoch) ready |= 1ull << (o0 + j);
             }
-            if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+            if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)origin << 32) | epoch);
           } while (!((ready >> origin) & 1ull)));
           fence_acq_rel_gpu();
           fence_proxy_async_global();
@@ -371,6 +371,11 @@ __global__ void __launch_bounds__(256, 1)
         pr[2] = w_flag;
       }
     }
+    // The other 31 lanes wait here (not in a spin loop of their own) until the producer lane
+    // is done: two divergent spin-wait paths in one warp can starve the role lane (found on
+    // hardware with the diagnostic watchdog: the tail issuer's flag polls never ran while its
+    // 31 lanes spun on e_load).
+    __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
     if (leader && elect_one()) {
@@ -467,6 +472,7 @@ __global__ void __launch_bounds__(256, 1)
         pr[8] = w_eempty;
       }
     }
+    __syncwarp();  // see warp 0
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs) =====================
     const int wq = warp & 3;
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(256, 1)
           for (int j = 0; j < 8; ++j)
             if (o0 + j < G && v[j] == epoch) seen |= 1ull << (o0 + j);
         }
-        if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+        if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED((seen << 32) | epoch);
       }
       fence_acq_rel_gpu();
       fence_proxy_async_global();
@@ -517,9 +523,14 @@ __global__ void __launch_bounds__(256, 1)
       const bool publish = G > 1 || !C::kOwnFull;  // the chunk goes to the L2 scratch
       constexpr int kRoundCols = C::kOWN_BYTES / (C::BM * 2);  // 128 columns per own-slot round
       const bool has = has_chunk(T, p);
+      // With the E/C column swap nothing waits for C(1)'s drain (no GEMM0(2); E already lives in
+      // C(0)'s columns), and arriving would let c_empty complete twice before the MMA thread's
+      // wait for C(0)'s drain looks -- a parity alias that hung a ragged member without chunks,
+      // whose two drains are both immediate (found on hardware by the diagnostic watchdog)
+      const bool release_c = !(swap_e && T == 1);
       if (!has) {  // ragged last n-step without a chunk here: the handshakes only
         tc_fence_before();
-        mbar_arrive_remote(L_c_empty);
+        if (release_c) mbar_arrive_remote(L_c_empty);
         if (C::kOwnFull) mbar_arrive_remote(L_own_full);
       }
 #pragma unroll 1
@@ -556,7 +567,7 @@ __global__ void __launch_bounds__(256, 1)
             for (int j = 0; j < 4; ++j) dst[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
           }
         }
-        if (r0 + kRoundCols >= C::kCW) {  // C accumulator fully read: GEMM0 of the next step may start
+        if (r0 + kRoundCols >= C::kCW && release_c) {  // C accumulator fully read: GEMM0 of the next step may start
           tc_fence_before();
           mbar_arrive_remote(L_c_empty);
         }
@@ -582,6 +593,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         mbar_arrive(own_free);
       }
+      __syncwarp();  // lanes 1-31 must not spin on the next barrier while the issuer publishes
       if (args.prof) t_store += clock64() - t_s0;
       if (issuer && T < 2) FF_STAMP(20 + 3 * T);
     };
@@ -785,7 +797,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int j = 0; j < S && FF_AB_TAIL != 2; ++j) {
         if (j == sp) continue;
         while (ld_relaxed_gpu_u32(slab_flag(j)) != epoch)
-          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+          if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)ld_relaxed_gpu_u32(slab_flag(j)) << 32) | epoch);
       }
       fence_acq_rel_gpu();
       fence_proxy_async_global();
@@ -797,6 +809,7 @@ __global__ void __launch_bounds__(256, 1)
             tma_load_3d(slot0 + j * (R * kChunks * 16), &maps.slab, e_load, 0, sp * R / 8, (tile * S + j) * kChunks);
       }
     }
+    __syncwarp();  // the issuer's lanes wait for it here, not spinning on e_load (it would starve the polls)
     if (FF_AB_TAIL != 2) mbar_wait(e_load, 0);
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
     // sum (deterministic order: own partial, then the partners in split order), cast,
@@ -864,7 +877,7 @@ __global__ void __launch_bounds__(256, 1)
       uint32_t polls = 0;
       for (int j = (int)lane_id(); j < G; j += 32)
         while (ld_relaxed_gpu_u32(done_flag(j)) != epoch)
-          if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+          if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)ld_relaxed_gpu_u32(done_flag(j)) << 32) | epoch);
       fence_acq_rel_gpu();
     }
     __syncthreads();

@@ -120,16 +120,38 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t par
 #define FF_WATCHDOG_POLLS (1u << 26)
 #endif
 __device__ __forceinline__ void watchdog_trap() { asm volatile("trap;"); }
+// Diagnostic builds (-DFF_DIAG_WATCHDOG, never the shipped library): an expired wait records
+// (source line, block, thread, info) in ff_diag and gives up instead of trapping, so the launch
+// completes and the host can read which wait hung (ff_diag_read).
+#ifdef FF_DIAG_WATCHDOG
+// ff_diag[0] = expired waits; then up to 512 (key, info) records in expiry order
+static __device__ unsigned long long ff_diag[1 + 2 * 512];
+__device__ __forceinline__ void watchdog_record(unsigned line, unsigned long long info) {
+  const unsigned long long key = ((unsigned long long)line << 40) | ((unsigned long long)blockIdx.x << 20) | threadIdx.x;
+  const unsigned long long i = atomicAdd(&ff_diag[0], 1ull);
+  if (i < 512) {
+    ff_diag[1 + 2 * i] = key;
+    ff_diag[2 + 2 * i] = info;
+  }
+}
+#define FF_WD_EXPIRED(info) \
+  {                         \
+    watchdog_record(__LINE__, (unsigned long long)(info)); \
+    break;                  \
+  }
+#else
+#define FF_WD_EXPIRED(info) watchdog_trap()
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t polls = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+    if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)bar << 8) | parity);
   }
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
   uint32_t polls = 0;
   while (!mbar_try_wait_cluster(bar, parity)) {
-    if (++polls == FF_WATCHDOG_POLLS) watchdog_trap();
+    if (++polls == FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)bar << 8) | 0x10 | parity);
   }
 }
 
@@ -150,7 +172,7 @@ __device__ __forceinline__ uint32_t ld_acquire_cluster_u32(uint32_t addr) {
 __device__ __forceinline__ void credit_wait(uint32_t addr, uint32_t target) {
   uint32_t polls = 0;
   while ((int)(ld_acquire_cluster_u32(addr) - target) < 0) {
-    if (++polls == 16 * FF_WATCHDOG_POLLS) watchdog_trap();
+    if (++polls == 16 * FF_WATCHDOG_POLLS) FF_WD_EXPIRED(((unsigned long long)addr << 32) | target);
   }
 }
 

@@ -12,6 +12,7 @@ def graph(kind, act, m, n, k, l):
     d = W.DimensionSpec(m, n, k, l, 2)
     return W.build_gated_ffn(d) if kind == 'gated_ffn' else W.build_standard_ffn(d, act)
 
+lib = nat.load()
 rng = random.Random(int(sys.argv[1]) if len(sys.argv) > 1 else 7)
 n_cases, fails, ran = int(sys.argv[2]) if len(sys.argv) > 2 else 60, 0, 0
 for i in range(n_cases):
@@ -44,6 +45,14 @@ for i in range(n_cases):
             fails += 1
             print('ERROR', kind, act, (m, n, k, l), 'f16' if f16 else 'bf16', x, cfg.as_dict(), e, flush=True)
             continue
+        if hasattr(lib, 'ff_diag_read'):  # diagnostic build (FF_CHAIN_LIB=...libff_diag.so): expired waits
+            import ctypes
+            d = (ctypes.c_ulonglong * 1025)()
+            lib.ff_diag_read(d)
+            if d[0]:
+                fails += 1
+                print('EXPIRED', kind, act, (m, n, k, l), x, cfg.as_dict(), d[0], 'first line', d[1] >> 40,
+                      'block', (d[1] >> 20) & 0xFFFFF, 'thread', d[1] & 0xFFFFF, hex(d[2]), flush=True)
         got = out.float().cpu().numpy()
         err = oracle.max_relative_error(got, ref)
         ran += 1

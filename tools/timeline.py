@@ -111,6 +111,12 @@ def main(argv):
                 col = col[col > 0]
                 if col.numel():
                     print(f"   {nm:15s} mean {col.mean().item() / 1e3:9.1f} max {col.max().item() / 1e3:9.1f} kcyc")
+        if 'members' in argv:  # last-MMA time (E_start) per ring member pair, to see systematic skew
+            g2 = kc.ring * 2
+            es = rel[:, 14]
+            for r in range(kc.rings):
+                vals = [es[r * g2 + 2 * p_: r * g2 + 2 * p_ + 2].mean().item() for p_ in range(kc.ring)]
+                print(f"   ring {r} E_start per member: " + " ".join(f"{x:5.1f}" for x in vals))
         if 'rings' in argv:
             g2 = kc.ring * 2
             for r in range(kc.rings):
