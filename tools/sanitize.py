@@ -21,6 +21,8 @@ CASES = [  # (kind, m, n, k, l, explicit CTA-pair config or None = auto lowering
     ("standard_ffn", 256, 2048, 512, 512, None),
     ("gated_ffn", 256, 1024, 512, 512, None),
     ("standard_ffn", 512, 1024, 256, 512, None),
+    # ragged pair ring whose last split has members without a chunk (E/C swap, empty drains)
+    ("standard_ffn", 17, 3328, 512, 512, None),
     # whole n-steps (non-ragged pair kernels; quads with an even m-tile count), split-N
     # reduce-scatter tail and the C-scratch discard
     ("standard_ffn", 512, 2048, 512, 512, dict(ring=2, n_splits=4, nb=256, lb=256, exchange=2)),
