@@ -196,6 +196,7 @@ void ff_set_profile_buffer(void* dev_ptr);
 #define FF_VARIANT_SCRATCH_DISCARD 0x100u    /* pair kernel: also discard the C exchange scratch at exit */
 #define FF_VARIANT_NO_SERP 0x200u            /* pair kernel: every unit walks its n-steps in order */
 #define FF_VARIANT_E_EVICT_FIRST 0x400u      /* pair kernel: E tile stores with L2 evict_first */
+#define FF_VARIANT_NO_TAIL_SPLIT 0x800u      /* pair kernel: keep the last partial wave's units whole */
 void ff_set_variant(uint32_t flags);
 
 /* Thread-local message for the last non-OK status. */

@@ -226,6 +226,9 @@ int table_active_clusters(int cluster, int num_sms) {
   return num_sms >= 148 ? n : (n * num_sms) / 148 > 0 ? (n * num_sms) / 148 : 1;
 }
 
+unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
+uint32_t g_variant = 0;  // kernel-variant selection for A/B runs and tests (ff_set_variant, FF_VARIANT_*)
+
 struct WsLayout {
   size_t e_off, c_off, f_off, n_off, s_off, total;
   bool e_memset;  // fp32 E larger than the zero zone: clear it before the launch
@@ -255,6 +258,19 @@ bool pair_ragged(const ffChainDesc* ch, const ffKernelConfig* c) {
 // one unit per ring keeps one slot per step.
 int pair_c_slots(const ffKernelConfig* c) {
   return c->units > c->rings ? 3 : std::min(3, std::max(1, (int)c->steps));
+}
+// Pair kernel, multi-unit S == 1 launches: the last wave holds rem = units % rings units and
+// would leave rings - rem rings idle; each of them is split in N into tail_S units (at most one
+// per ring) of steps / tail_S n-steps that combine through the split-N reduce-scatter
+// (OPT M=32768: 128 units on 9 rings, rem 2 -> 8 quarter units: 14.25 waves instead of 15).
+int pair_tail_splits(const ffChainDesc* ch, const ffKernelConfig* c) {
+  if (g_variant & FF_VARIANT_NO_TAIL_SPLIT) return 1;
+  if (c->n_splits != 1 || c->l_clusters != 1 || c->units <= c->rings || pair_ragged(ch, c)) return 1;
+  const int rem = c->units % c->rings;
+  if (rem == 0) return 1;
+  for (int st : {8, 4, 2})
+    if (rem * st <= c->rings && c->steps % st == 0) return st;
+  return 1;
 }
 
 WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = false) {
@@ -286,12 +302,12 @@ WsLayout ws_layout(const ffChainDesc* ch, const ffKernelConfig* c, bool conv2 = 
   w.s_off = off;
   if (c->n_splits > 1 && !dsmr)  // split-N exchange regions (pair kernel, and the 1-CTA kernels' final units)
     off = align256(off + (size_t)c->n_splits * (size_t)c->m_tiles * (pair ? 256 : 128) * ch->l * sizeof(float));
+  else if (pair && pair_tail_splits(ch, c) > 1)  // tail units: regions for the last wave's m tiles only
+    off = align256(off + (size_t)pair_tail_splits(ch, c) * (size_t)(c->units % c->rings) * 256 * ch->l * sizeof(float));
   w.total = off;
   return w;
 }
 
-unsigned long long* g_prof = nullptr;  // diagnostics: per-CTA counters + timeline (ff_set_profile_buffer)
-uint32_t g_variant = 0;  // kernel-variant selection for A/B runs and tests (ff_set_variant, FF_VARIANT_*)
 
 // Split-N finish by exchange regions (pair kernel): one unit per ring, S | 128
 // with 8-row slices, and the slab flags of every E tile fit their region.
@@ -537,15 +553,22 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // eleven of them costs several microseconds of host time per launch, so the
   // last few sets are kept per thread and reused when a caller launches again
   // on the same buffers (serving loops, benchmarks, graph capture).
+  // tail split of the last partial wave: planned on cfg->rings (the workspace layout's
+  // basis); used only when that many rings are co-resident
+  const int tail_S = pair_tail_splits(ch, cfg);
   struct Key {
     ffChainDesc ch;
-    int32_t ring, n_splits, nb, lb, m_tiles;
+    int32_t ring, n_splits, nb, lb, m_tiles, units, rings, steps, tail;
     const void *a, *b, *b1, *d;
     void *e, *ws;
   };
   Key key;
   std::memset(&key, 0, sizeof(key));
   key.ch = *ch;
+  key.units = cfg->units;
+  key.rings = cfg->rings;
+  key.steps = cfg->steps;
+  key.tail = tail_S;
   key.ring = cfg->ring;
   key.n_splits = cfg->n_splits;
   key.nb = cfg->nb;
@@ -619,7 +642,8 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   {  // whole-tile / row-slice 3D views of E and the fp32 workspace (final-unit epilogue)
     // split row slice (the reduce-scatter tail needs S <= 8, pair_finish_regions; the maps
     // are encoded for every launch, so keep their boxes legal for any S)
-    const uint32_t rs = std::max(1u, 128u / (uint32_t)std::max(1, cfg->n_splits));
+    const int s_eff = tail_S > 1 ? tail_S : std::max(1, cfg->n_splits);  // splits meeting in the tail
+    const uint32_t rs = std::max(1u, 128u / (uint32_t)s_eff);
     const uint64_t de[3] = {64, M, L / 64}, se[2] = {L * 2, 128};
     const uint32_t be[3] = {64, 128, 256 / 64}, ber[3] = {64, rs, 256 / 64};
     ok = ok && make_map_nd(&maps.e3, BF, 3, t->e, de, se, be);
@@ -631,9 +655,10 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
     // split-N exchange regions [E tile][split][16-byte chunk][128 rows] x 16 B as a 3D
     // {8 rows x 4 floats, 16 row groups, chunk}: box {32, 128/S/8, 64} = one split's
     // rows of a slice, 128-byte inner rows (lands as [chunk][row][16 B] in smem)
-    const uint64_t S = (uint64_t)std::max(1, cfg->n_splits);
-    const void* sp = cfg->n_splits > 1 ? (const void*)(wsb + wl.s_off) : t->e;
-    const uint64_t tiles = (uint64_t)cfg->m_tiles * 2 * (L / 256);
+    const uint64_t S = (uint64_t)s_eff;
+    const void* sp = s_eff > 1 ? (const void*)(wsb + wl.s_off) : t->e;
+    // tail units: regions for the last wave's m tiles only (ws_layout)
+    const uint64_t tiles = (uint64_t)(tail_S > 1 ? cfg->units % cfg->rings : cfg->m_tiles) * 2 * (L / 256);
     const uint64_t ds[3] = {32, 16, tiles * S * 64}, ss[2] = {128, 2048};
     const uint32_t bs[3] = {32, std::max(1u, rs / 8), 64};
     ok = ok && make_map_nd(&maps.slab, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sp, ds, ss, bs, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -671,6 +696,16 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.l_clusters = cfg->l_clusters;
   a.n_units = cfg->units;
   a.n_rings = rings;
+  // tail split (pair_tail_splits): plain pairs only (quad twins must share weights), and only
+  // on the planned ring count the workspace was laid out for
+  if (!kQuad && tail_S > 1 && rings == cfg->rings) {
+    a.tail_S = tail_S;
+    a.n_full = cfg->units - cfg->units % rings;
+    a.n_units = a.n_full + (cfg->units % rings) * tail_S;
+  } else {
+    a.tail_S = 1;
+    a.n_full = cfg->units;
+  }
   a.act = ch->activation;
   a.dev_epoch = reinterpret_cast<uint32_t*>(wsb + wl.f_off) + (kFlagBytes / 4 - 1);  // last flag-region word
   a.exit_cnt = reinterpret_cast<uint32_t*>(wsb + wl.n_off) + (kCntBytes / 4 - 1);    // last counter word
@@ -766,7 +801,9 @@ int launch_pair_q(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffTens
   // ragged n-steps (N not a whole number of ring steps per split): plain pairs only
   if (ch->n != (int64_t)cfg->n_splits * cfg->steps * cfg->ring * cfg->nb)
     return launch_pair_impl<kGated, kPacked, false, true>(ch, cfg, t, ws, c_debug, stream, conv);
-  return quad_ok(cfg, kGated) ? launch_pair_impl<kGated, kPacked, true, false>(ch, cfg, t, ws, c_debug, stream, conv)
+  // (a tail-split launch needs plain pairs: quad twins share weight tiles, tail units do not)
+  return quad_ok(cfg, kGated) && pair_tail_splits(ch, cfg) == 1
+             ? launch_pair_impl<kGated, kPacked, true, false>(ch, cfg, t, ws, c_debug, stream, conv)
                       : launch_pair_impl<kGated, kPacked, false, false>(ch, cfg, t, ws, c_debug, stream, conv);
 }
 

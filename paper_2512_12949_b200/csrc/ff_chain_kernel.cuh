@@ -78,6 +78,8 @@ struct ChainArgs {
   int epolicy;         // pair kernel: L2 hint for the E tile stores (E is never re-read by the kernel)
   int split_cl;        // L2 kernels: the S N splits of an E tile are one thread-block cluster and combine
                        // their fp32 partials by a DSM reduce-scatter (FF_XCHG_L2_DSMR)
+  int tail_S;          // pair kernel: > 1 splits the last partial wave's units in N into tail_S units each
+  int n_full;          // pair kernel, tail_S > 1: units before the tail units (a whole number of waves)
   int serp;            // pair kernel: a ring's odd units run their n-steps in reverse order, so the
                        // weights the previous unit read last (still in L2) are read first
   int discard;         // pair kernel: drop dead scratch from L2 without a DRAM write-back once its last

@@ -106,13 +106,29 @@ __global__ void __launch_bounds__(256, 1)
   const int krot = args.krot ? (p * kblocks / G) : 0;
   const int steps = args.steps;
   const int my_units = ring < args.n_units ? (args.n_units - ring + args.n_rings - 1) / args.n_rings : 0;
-  const int total_steps = my_units * steps;
+  // Tail split (multi-unit launches, S == 1, one l cluster): the units of the last, partial wave
+  // would leave rings idle, so each is cut in N into tail_S units of steps / tail_S n-steps
+  // (units n_full.. in that order, at most one per ring, always the ring's last) that combine
+  // through the split-N reduce-scatter.  A ring's global step T then maps to (unit, step)
+  // with a shorter last unit.
+  const bool has_tail = args.tail_S > 1 && my_units > 0 && ring + (my_units - 1) * args.n_rings >= args.n_full;
+  const int steps_t = args.tail_S > 1 ? steps / args.tail_S : steps;
+  const int full_steps = (my_units - (has_tail ? 1 : 0)) * steps;
+  const int total_steps = full_steps + (has_tail ? steps_t : 0);
+  auto ui_of = [&](int T) { return T < full_steps ? T / steps : my_units - 1; };
+  auto t_of = [&](int T) { return T < full_steps ? T % steps : T - full_steps; };
+  auto steps_of = [&](int ui) { return (has_tail && ui == my_units - 1) ? steps_t : steps; };
 
   struct Unit {
     int m0, l0, n0, id, split;
   };
   auto unit_of = [&](int i) {
     const int u = ring + i * args.n_rings;
+    if (args.tail_S > 1 && u >= args.n_full) {  // tail unit: split (u - n_full) % tail_S of m tile n_full + ..
+      const int j = u - args.n_full;
+      return Unit{(args.n_full + j / args.tail_S) * 2 * C::BM, p * kLB, (j % args.tail_S) * steps_t * G * C::kN0, u,
+                  j % args.tail_S};
+    }
     const int mt = u % args.m_tiles;
     const int rest = u / args.m_tiles;
     const int lc = rest % args.l_clusters;
@@ -128,14 +144,14 @@ __global__ void __launch_bounds__(256, 1)
   // n-steps backwards (serpentine), so the first weights they read are the ones the
   // previous unit read last.  Flags, scratch slots and the schedule keep the logical step.
   auto nstep = [&](int T) {
-    const int t = T % steps;
-    return (!kRagged && args.serp && ((T / steps) & 1)) ? steps - 1 - t : t;
+    const int t = t_of(T), ui = ui_of(T);
+    return (!kRagged && args.serp && (ui & 1)) ? steps_of(ui) - 1 - t : t;
   };
   auto has_chunk = [&](int T, int origin) {
     if (!kRagged) return true;
-    const int split = unit_of(T / steps).split;
+    const int split = unit_of(ui_of(T)).split;
     const int lim = min(args.split_chunks, args.total_chunks - split * args.split_chunks);
-    return (T % steps) * G + origin < lim;
+    return t_of(T) * G + origin < lim;
   };
 
   const uint32_t bar0 = base + C::kOFF_BAR;
@@ -224,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
                  L_e_empty = mapa(e_empty, lrank);
   // Split-N reduce-scatter tail (one unit per ring, S > 1): all eight warps
   // drain the ring's last E partial after the role loops (see below).
-  const bool scatter_all = args.S > 1 && args.finish_tma && total_steps > 0;
+  const bool scatter_all = (args.S > 1 && args.finish_tma && total_steps > 0) || has_tail;
   // C scratch discard at exit (one set of regions per ring, addressed per member and slot)
   const bool discard_c = (args.discard & 2) && !kRagged && (G > 1 || !C::kOwnFull) && my_units > 0;
   auto done_flag = [&](int member) { return args.flags + (3u << 16) + ring * G + member; };
@@ -256,11 +272,18 @@ __global__ void __launch_bounds__(256, 1)
       auto arm = [&]() {
         if (leader) mbar_expect_tx(full_bar(stage), 2 * C::kSTAGE);
       };
-      auto load_gemm0 = [&](int T, int kb0, int kb1) {
+      // (unit, step, physical n-step) of a global step, computed once per step: the per-hop
+      // integer divisions of the mapping sat on the producer's critical path (+10 us, A/B)
+      struct StepAt {
+        Unit u;
+        int t, ns;
+      };
+      auto step_at = [&](int T) { return StepAt{unit_of(ui_of(T)), t_of(T), nstep(T)}; };
+      auto load_gemm0 = [&](int T, const StepAt& st, int kb0, int kb1) {
         if (kb0 >= kb1 || !has_chunk(T, p)) return;
-        const Unit u = unit_of(T / steps);
+        const Unit& u = st.u;
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
-        const int nblk = (u.n0 + (nstep(T) * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
+        const int nblk = (u.n0 + (st.ns * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
         for (int kbl = kb0; kbl < kb1; ++kbl) {
           const int kb = (kbl + krot) % kblocks;  // physical k-block (members start at staggered k)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
@@ -305,11 +328,11 @@ __global__ void __launch_bounds__(256, 1)
         }
       };
       unsigned long long ready = 0;  // ring members whose C chunk of the current step is published
-      auto load_hop = [&](int T, int h) {
-        const Unit u = unit_of(T / steps);
-        const int t = T % steps;
+      auto load_hop = [&](int T, const StepAt& st, int h) {
+        const Unit& u = st.u;
+        const int t = st.t;
         const int origin = (p - h + G) % G;
-        const int ncol0 = u.n0 + (nstep(T) * G + origin) * C::kN0;
+        const int ncol0 = u.n0 + (st.ns * G + origin) * C::kN0;
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
         if (h == 0) ready = C::kOwnFull ? 1ull << p : 0ull;
@@ -339,7 +362,7 @@ __global__ void __launch_bounds__(256, 1)
           fence_proxy_async_global();
         }
         if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
-          const int ncol_pf = u.n0 + (nstep(T) * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
+          const int ncol_pf = u.n0 + (st.ns * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
             tma_prefetch_l2_3d_h(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk, pol_w);
         }
@@ -357,12 +380,15 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
       };
-      if (total_steps > 0) load_gemm0(0, 0, kblocks);
+      StepAt cur = step_at(0);
+      if (total_steps > 0) load_gemm0(0, cur, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
+        const StepAt nxt = T + 1 < total_steps ? step_at(T + 1) : cur;
         for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          load_hop(T, h);
+          if (T + 1 < total_steps) load_gemm0(T + 1, nxt, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
+          load_hop(T, cur, h);
         }
+        cur = nxt;
       }
       if (args.prof) {
         unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
@@ -419,10 +445,8 @@ __global__ void __launch_bounds__(256, 1)
         if (kb1 == kblocks) umma_commit_pair((swap_e && T == 1) ? c_full1 : c_full, kPairMask);
       };
       bool e_started = false;
-      auto hop = [&](int T, int h) {
-        const int t = T % steps;
+      auto hop = [&](int T, int t, int ui, int h) {
         if (t == 0 && h == 0) {
-          const int ui = T / steps;
           if (ui > 0) {
             FF_TIMED(w_eempty, mbar_wait_cluster(e_empty, (ui - 1) & 1));
             tc_fence_after();
@@ -450,13 +474,14 @@ __global__ void __launch_bounds__(256, 1)
           next();
         }
         if (C::kOwnFull && h == 0) umma_commit_pair(own_free, kPairMask);
-        if (t == steps - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
+        if (t == steps_of(ui) - 1 && h == G - 1) umma_commit_pair(e_full, kPairMask);
       };
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
+        const int t = t_of(T), ui = ui_of(T);  // once per step (see the producer)
         for (int h = 0; h < G; ++h) {
           if (T + 1 < total_steps) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
-          hop(T, h);
+          hop(T, t, ui, h);
         }
       }
       // every C load of this pair has landed (its full barriers completed): the ring's
@@ -490,8 +515,8 @@ __global__ void __launch_bounds__(256, 1)
     auto wait_slot_free = [&](int T) {
       if (kRagged || T < args.c_slots) return;
       const int Tp = T - args.c_slots + 2;
-      const Unit up = unit_of(Tp / steps);
-      const int tp = Tp % steps;
+      const Unit up = unit_of(ui_of(Tp));
+      const int tp = t_of(Tp);
       uint32_t polls = 0;
       unsigned long long seen = 0ull;
       const unsigned long long all = G >= 64 ? ~0ull : (1ull << G) - 1ull;
@@ -513,8 +538,8 @@ __global__ void __launch_bounds__(256, 1)
     };
     // C chunk of global step T: TMEM -> activation / gate -> bf16 SW128 own slot -> L2 scratch + flag
     auto drain_c = [&](int T) {
-      const Unit u = unit_of(T / steps);
-      const int t = T % steps;
+      const Unit u = unit_of(ui_of(T));
+      const int t = t_of(T);
       FF_TIMED(w_cfull, (swap_e && T == 1) ? mbar_wait_cluster(c_full1, 0) : mbar_wait_cluster(c_full, T & 1));
       tc_fence_after();
       if (issuer && T < 2) FF_STAMP(18 + 3 * T);
@@ -603,9 +628,9 @@ __global__ void __launch_bounds__(256, 1)
         drain_c(T);
         next_c = T + 1;
       }
-      const Unit u = unit_of(T / steps);
-      const int t = T % steps;
-      if (t == steps - 1 && !(scatter_all && T == total_steps - 1)) {
+      const Unit u = unit_of(ui_of(T));
+      const int t = t_of(T);
+      if (t == steps_of(ui_of(T)) - 1 && !(scatter_all && T == total_steps - 1)) {
         // The next unit's first C chunk is ready mid-way through this unit's last hops:
         // drain and publish it before this unit's E, so the tensor core can start the
         // next GEMM0 while E drains (not with kOwnFull: the own slot then still holds
@@ -617,7 +642,7 @@ __global__ void __launch_bounds__(256, 1)
         // E slice: TMEM -> registers -> SW128 smem tiles in the own slot -> TMA
         // store (bf16) or TMA reduce-add into the fp32 workspace (N splits).
         const unsigned long long t_e0 = args.prof ? clock64() : 0ull;
-        mbar_wait_cluster(e_full, (T / steps) & 1);
+        mbar_wait_cluster(e_full, ui_of(T) & 1);
         tc_fence_after();
         if (issuer) FF_STAMP(30);
         mbar_wait_cluster(own_free, (next_c - 1) & 1);  // own slot no longer read by hop 0 / the last C store
@@ -626,7 +651,7 @@ __global__ void __launch_bounds__(256, 1)
         // unit, when every pipeline stage has been consumed (e_full) and no
         // further load is coming -- the whole stage area, so the E tile leaves
         // in one round of TMA stores / reduce-adds.
-        const bool final_unit = (T / steps) == my_units - 1;
+        const bool final_unit = ui_of(T) == my_units - 1;
         const uint32_t stg = final_unit ? base : own_slot;
         const int kTiles = final_unit ? (kStages * C::kSTAGE) / 16384 : C::kOWN_BYTES / 16384;
         const bool bf16_out = (args.S == 1);
@@ -747,7 +772,7 @@ __global__ void __launch_bounds__(256, 1)
     // bf16 and stage the rows for one TMA store of E.  Warp w reads TMEM lane
     // quarter w%4; warps 0-3 take the upper half of the columns.
     const Unit u = unit_of(my_units - 1);
-    const int S = args.S, R = C::BM / S, sp = u.split;
+    const int S = has_tail ? args.tail_S : args.S, R = C::BM / S, sp = u.split;
     const int erow = u.m0 + (int)q * C::BM;
     const int wq = warp & 3;
     const int row = wq * 32 + (int)lane_id();
@@ -756,12 +781,17 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t lane_base = tmem_base + ((uint32_t)(wq * 32) << 16);
     const int c_lo = warp < 4 ? kLB / 2 : 0;
     const int slice = row / R;
-    const int tile = (erow / C::BM) * (args.L / kLB) + u.l0 / kLB;
+    // E tile index of the exchange regions / flags (tail units: counted from the first tail m tile)
+    const int tile = ((erow - (has_tail ? args.n_full * 2 * C::BM : 0)) / C::BM) * (args.L / kLB) + u.l0 / kLB;
     // exchange region of (tile, split s): [kChunks][128 rows] x 16 B
     auto region = [&](int s_) { return args.slab + ((size_t)tile * S + s_) * (kChunks * 128 * 4); };
     auto slab_flag = [&](int s_) { return args.flags + (1u << 17) + tile * 16 + s_; };
-    mbar_wait_cluster(e_full, (my_units - 1) & 1);
-    __syncwarp();  // warps 0/1 arrive from divergent role loops; tcgen05.ld is warp-collective
+    // Only the epilogue warps, which observed every earlier completion of e_full in order, wait
+    // for the last unit's: a warp that has not would read parity (my_units - 1) & 1 against a
+    // barrier still in an earlier phase (with a tail unit, parity 1 before the first completion
+    // passes at once -- found on hardware: the tail's upper column halves were read too early).
+    if (warp >= 4) mbar_wait_cluster(e_full, (my_units - 1) & 1);
+    __syncthreads();
     tc_fence_after();
     if (issuer) FF_STAMP(30);
     // shared memory (drained stages): slot j != sp = [kChunks][R rows][16 B] partner j's

@@ -187,6 +187,7 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
     tp = nat.Tensors(a.data_ptr(), tensors["B0" if gated else "B"].data_ptr(),
                      tensors["B1"].data_ptr() if gated else None, tensors["D"].data_ptr(), out.data_ptr())
     ws_ptr = ws.data_ptr() if ws is not None else None
+    ws_bytes = ws.numel() if ws is not None else 0  # the buffer's size: the library checks it covers the layout
     if c_debug is not None:
         rc = lib.ff_chain_launch_debug(ctypes.byref(ch), ctypes.byref(cfg), ctypes.byref(tp), ws_ptr, ws_bytes,
                                        c_debug.data_ptr(), handle)

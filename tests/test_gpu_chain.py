@@ -278,6 +278,32 @@ def test_pair_kernel_serpentine_units_match_oracle(mode):
     _check(kind, act, host, out)
 
 
+# tail split: the last partial wave's units are cut in N across the idle rings and combined by the
+# split-N reduce-scatter (11 units of 4 n-steps on 9 rings: 9 whole units + 2 x 4 quarter units),
+# against the oracle with and without it, and bitwise repeatable
+@pytest.mark.parametrize("mode", [0x0, 0x800], ids=["tail-split", "no-tail-split"])
+def test_pair_kernel_tail_split_matches_oracle(mode):
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = "standard_ffn", "relu", 11 * 256, 8192, 512, 2048
+    graph = _graph(kind, act, m, n, k, l)
+    host, dev = _inputs(kind, m, n, k, l, seed=17)
+    lib = nat.load()
+    lib.ff_set_variant(mode)
+    try:
+        cfg = runtime.lower(graph, None, 148, "pair")
+        assert cfg.units == 11 and cfg.rings == 9 and cfg.steps == 4
+        out1 = runtime.launch(graph, cfg, dev).clone()
+        out2 = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+    finally:
+        lib.ff_set_variant(0)
+    _check(kind, act, host, out1)
+    assert torch.equal(out1, out2), "the tail split's reduce-scatter must be deterministic"
+
+
 def _random_cases(n, seed):
     rng = __import__("random").Random(seed)
     cases = []

@@ -27,6 +27,9 @@ def main(argv):
     def flush():
         flush_buf.add_(1.0)
 
+    # variants may lay the workspace out differently (the tail split adds exchange regions):
+    # one workspace large enough for all of them
+    runtime._workspace(1 << 30, torch.device("cuda", 0), torch.cuda.current_stream())
     for name in names:
         kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
         t = bench.make_device_inputs(kind, m, n, k, l, seed=1, device="cuda")
