@@ -207,9 +207,10 @@ __global__ void __launch_bounds__(256, 1)
   // (one slice: GEMM0(T+1) before every hop of step T); the ring's last GEMM0
   // always runs that way (defer_last): nothing follows it, so all hops are
   // needed to cover its drain, publish and the ring members' skew.
+  auto g0_slices = [&](int Tn) { return (Tn == total_steps - 1 && args.defer_last) ? 1 : G - args.defer; };
   auto slot_lo = [&](int Tn, int h) {
-    const int g0_slices = (Tn == total_steps - 1 && args.defer_last) ? 1 : G - args.defer;
-    return h < g0_slices ? h * kblocks / g0_slices : kblocks;
+    const int g0s = g0_slices(Tn);
+    return h < g0s ? h * kblocks / g0s : kblocks;
   };
   // One unit of two n-steps (the M=512 chains): GEMM0(1) runs before any hop of
   // step 0, while the E accumulator is still unused, so it accumulates in E's TMEM
@@ -285,7 +286,9 @@ __global__ void __launch_bounds__(256, 1)
         // first 64-column block of this CTA's half of the chunk (gated: of each branch)
         const int nblk = (u.n0 + (st.ns * G + p) * C::kN0) / 64 + (int)q * (C::kN0 / 128);
         for (int kbl = kb0; kbl < kb1; ++kbl) {
-          const int kb = (kbl + krot) % kblocks;  // physical k-block (members start at staggered k)
+          // physical k-block (members start at staggered k); no runtime division on the producer's
+          // per-stage path (its issue latency is the pipeline's, see StepAt)
+          const int kb = kbl + krot < kblocks ? kbl + krot : kbl + krot - kblocks;
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(256, 1)
           const int pf = args.prefetch;
 #endif
           if (pf && kbl + pf < kblocks && (!kQuad || pq == 0)) {
-            const int kbp = (kbl + pf + krot) % kblocks;
+            const int kbp = kbl + pf + krot < kblocks ? kbl + pf + krot : kbl + pf + krot - kblocks;
             if (!kGated || !kPackedB)
               tma_prefetch_l2_3d_h(&maps.b, 0, kbp * C::BK, nblk, pol_w);
             else
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(256, 1)
       auto load_hop = [&](int T, const StepAt& st, int h) {
         const Unit& u = st.u;
         const int t = st.t;
-        const int origin = (p - h + G) % G;
+        const int origin = p >= h ? p - h : p - h + G;
         const int ncol0 = u.n0 + (st.ns * G + origin) * C::kN0;
         const int dblk = u.l0 / 64 + (int)q * (kLB / 128);
         const bool from_l2 = h > 0 || !C::kOwnFull;  // C operand of this hop comes from the L2 scratch
@@ -362,17 +365,19 @@ __global__ void __launch_bounds__(256, 1)
           fence_proxy_async_global();
         }
         if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
-          const int ncol_pf = u.n0 + (st.ns * G + (p - h - args.prefetch + 2 * G) % G) * C::kN0;
+          const int o_pf = p - h - args.prefetch + (p - h - args.prefetch < -G ? 2 * G : p - h - args.prefetch < 0 ? G : 0);
+          const int ncol_pf = u.n0 + (st.ns * G + o_pf) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
             tma_prefetch_l2_3d_h(&maps.d, 0, ncol_pf + kb2 * C::BK, dblk, pol_w);
         }
+        const int crow = c_row(u, T, origin), cblk = c_blk(u, t, origin);  // once per hop
         for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2) {
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
           if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
           if (from_l2)
-            tma_load_3d_pair_h(sb, &maps.c, lb, 0, c_row(u, T, origin), c_blk(u, t, origin) + kb2 * (C::BK / 64), pol_c);
+            tma_load_3d_pair_h(sb, &maps.c, lb, 0, crow, cblk + kb2 * (C::BK / 64), pol_c);
           if (!kQuad)
             tma_load_3d_pair_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, pol_w);
           else if ((seq++ & 1u) == pq)
@@ -384,8 +389,10 @@ __global__ void __launch_bounds__(256, 1)
       if (total_steps > 0) load_gemm0(0, cur, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         const StepAt nxt = T + 1 < total_steps ? step_at(T + 1) : cur;
+        const int g0s = g0_slices(T + 1);
         for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) load_gemm0(T + 1, nxt, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
+          // (the slice bounds only for the hops that carry GEMM0(T+1) k-blocks: slot_lo divides)
+          if (T + 1 < total_steps && h < g0s) load_gemm0(T + 1, nxt, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
           load_hop(T, cur, h);
         }
         cur = nxt;
@@ -479,8 +486,9 @@ __global__ void __launch_bounds__(256, 1)
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
         const int t = t_of(T), ui = ui_of(T);  // once per step (see the producer)
+        const int g0s = g0_slices(T + 1);
         for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
+          if (T + 1 < total_steps && h < g0s) gemm0(T + 1, slot_lo(T + 1, h), slot_lo(T + 1, h + 1));
           hop(T, t, ui, h);
         }
       }
