@@ -250,9 +250,15 @@ __global__ void __launch_bounds__(256, 1)
   auto b_desc = [](uint32_t slot, int kk) { return desc_mnmajor_sw128(slot + kk * 2048, 16384); };
   constexpr int kChunks = kLB / 4;  // 16-byte column chunks per E row
 
-  if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
-    if (elect_one()) {
+#ifndef FF_PRODUCER_SPLIT  // 1: two producer threads (warp 0: A / C + barrier arming + flags; warp 2: weights)
+#define FF_PRODUCER_SPLIT 1
+#endif
+  // TMA producer body.  role 0 issues the A / C boxes, arms the full barriers and polls the
+  // ready flags; role 1 issues the weight boxes (B / gate|up, D) and their L2 prefetches;
+  // role 2 does both.  Both threads of a split walk the same stage sequence.
+  auto producer = [&](const int role) {
+    const bool do_ac = role != 1, do_w = role != 0;
+    {
       unsigned long long w_empty = 0, w_flag = 0;
       const unsigned long long t_start = clock64();
       int stage = 0, phase = 0;
@@ -292,8 +298,14 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
-          arm();
-          tma_load_3d_pair(sb, &maps.a, lb, 0, u.m0 + (int)q * C::BM, kb * (C::BK / 64));
+          if (do_ac) {
+            arm();
+            tma_load_3d_pair(sb, &maps.a, lb, 0, u.m0 + (int)q * C::BM, kb * (C::BK / 64));
+          }
+          if (!do_w) {
+            next();
+            continue;
+          }
           const bool mine = !kQuad || ((seq++ & 1u) == pq);  // this pair issues the shared weight tile
           // L2 prefetch of the B tile `prefetch` k-blocks ahead: the weights
           // stream from HBM; the extra lead hides its latency behind 3 stages
@@ -343,7 +355,7 @@ __global__ void __launch_bounds__(256, 1)
 #ifdef FF_AB_NO_FLAG_WAIT  // A/B builds only: cost of the ready-flag polls (results are not valid)
         if (false) {
 #else
-        if (from_l2 && !((ready >> origin) & 1ull)) {
+        if (do_ac && from_l2 && !((ready >> origin) & 1ull)) {
 #endif
           // one round trip polls every member whose chunk is still missing
           uint32_t polls = 0;
@@ -364,7 +376,7 @@ __global__ void __launch_bounds__(256, 1)
           fence_acq_rel_gpu();
           fence_proxy_async_global();
         }
-        if (args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
+        if (do_w && args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
           const int o_pf = p - h - args.prefetch + (p - h - args.prefetch < -G ? 2 * G : p - h - args.prefetch < 0 ? G : 0);
           const int ncol_pf = u.n0 + (st.ns * G + o_pf) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
@@ -375,13 +387,16 @@ __global__ void __launch_bounds__(256, 1)
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           const uint32_t lb = mapa(full_bar(stage), lrank);
-          if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
-          if (from_l2)
-            tma_load_3d_pair_h(sb, &maps.c, lb, 0, crow, cblk + kb2 * (C::BK / 64), pol_c);
-          if (!kQuad)
-            tma_load_3d_pair_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, pol_w);
-          else if ((seq++ & 1u) == pq)
-            tma_load_3d_pair_mcast_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, mcast, pol_w);
+          if (do_ac) {
+            if (leader) mbar_expect_tx(full_bar(stage), 2 * (from_l2 ? C::kSTAGE : C::kSLOT));
+            if (from_l2) tma_load_3d_pair_h(sb, &maps.c, lb, 0, crow, cblk + kb2 * (C::BK / 64), pol_c);
+          }
+          if (do_w) {
+            if (!kQuad)
+              tma_load_3d_pair_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, pol_w);
+            else if ((seq++ & 1u) == pq)
+              tma_load_3d_pair_mcast_h(sb + C::kSLOT, &maps.d, lb, 0, ncol0 + kb2 * C::BK, dblk, mcast, pol_w);
+          }
           next();
         }
       };
@@ -397,13 +412,20 @@ __global__ void __launch_bounds__(256, 1)
         }
         cur = nxt;
       }
-      if (args.prof) {
+      if (args.prof && do_ac) {
         unsigned long long* pr = args.prof + vcta * FF_PROF_STRIDE;
         pr[0] = clock64() - t_start;
         pr[1] = w_empty;
         pr[2] = w_flag;
       }
     }
+  };
+  // Split only rings of several units (measured, interleaved timelines: OPT M=32768 -3.5 %,
+  // M=4096 -1 %; one-unit rings: GPT-6.7B +0.6 %, LLaMA-1B +3-6 %)
+  const bool split_producer = FF_PRODUCER_SPLIT && my_units > 1;
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (elect_one()) producer(split_producer ? 0 : 2);
     // The other 31 lanes wait here (not in a spin loop of their own) until the producer lane
     // is done: two divergent spin-wait paths in one warp can starve the role lane (found on
     // hardware with the diagnostic watchdog: the tail issuer's flag polls never ran while its
@@ -505,6 +527,10 @@ __global__ void __launch_bounds__(256, 1)
         pr[8] = w_eempty;
       }
     }
+    __syncwarp();  // see warp 0
+  } else if (warp == 2 && split_producer) {
+    // ===================== TMA producer, weight boxes (both CTAs) =====================
+    if (elect_one()) producer(1);
     __syncwarp();  // see warp 0
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs) =====================
