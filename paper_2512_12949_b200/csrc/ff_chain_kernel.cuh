@@ -386,7 +386,14 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) FF_STAMP(17);
 
   // slot h of global step T holds GEMM0 k-blocks [h*KB/G, (h+1)*KB/G) of step T+1
-  auto slot_lo = [&](int h) { return h * kblocks / G; };
+  // GEMM0 slice [h * kblocks / G, (h + 1) * kblocks / G) of hop h, walked incrementally (no
+  // division per hop: the producer's and the MMA thread's issue latency is the pipeline's)
+  struct Slices {
+    int lo, hi, rem, q, r, G;
+    __device__ void start() { lo = 0, hi = q, rem = r; if (rem >= G) rem -= G, ++hi; }
+    __device__ void step() { lo = hi, hi += q, rem += r; if (rem >= G) rem -= G, ++hi; }
+  };
+  const Slices sl0{0, 0, 0, kblocks / G, kblocks % G, G};
   auto flag_addr = [&](const Unit& u, int t, int origin) {
     return args.flags + ((size_t)u.id * steps + t) * G + origin;
   };
@@ -407,7 +414,8 @@ __global__ void __launch_bounds__(256, 1)
         const Unit u = unit_of(T / steps);
         const int n0 = u.n0 + ((T % steps) * G + (int)p) * kNB;
         for (int kbl = kb0; kbl < kb1; ++kbl) {
-          const int kb = (kbl + krot) % kblocks;  // staggered k order across ring members
+          // staggered k order across ring members (no runtime division on the per-stage path)
+          const int kb = kbl + krot < kblocks ? kbl + krot : kbl + krot - kblocks;
           FF_TIMED(w_empty, mbar_wait(empty_bar(stage), phase ^ 1));
           const uint32_t sb = base + stage * C::kSTAGE;
           mbar_expect_tx(full_bar(stage), C::kG0_BYTES);
@@ -460,7 +468,7 @@ __global__ void __launch_bounds__(256, 1)
           }
           return;
         }
-        const int origin = ((int)p - h + G) % G;
+        const int origin = (int)p >= h ? (int)p - h : (int)p - h + G;
         const int nrow0 = u.n0 + (t * G + origin) * kNB;
         const bool remote_c = !kDSM && h > 0;
         if (remote_c) {
@@ -483,8 +491,10 @@ __global__ void __launch_bounds__(256, 1)
       };
       if (total_steps > 0) load_gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
-        for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) load_gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
+        Slices sl = sl0;
+        sl.start();
+        for (int h = 0; h < G; ++h, sl.step()) {
+          if (T + 1 < total_steps) load_gemm0(T + 1, sl.lo, sl.hi);
           load_hop(T, h);
         }
       }
@@ -544,8 +554,7 @@ __global__ void __launch_bounds__(256, 1)
       };
       int ri = 0;
       bool e_started = false;
-      auto hop = [&](int T, int h) {
-        const int t = T % steps;
+      auto hop = [&](int T, int t, int h) {
         if (t == 0 && h == 0) {
           // new unit: the epilogue must have drained the previous unit's E tile
           const int ui = T / steps;
@@ -593,9 +602,12 @@ __global__ void __launch_bounds__(256, 1)
       };
       if (total_steps > 0) gemm0(0, 0, kblocks);
       for (int T = 0; T < total_steps; ++T) {
-        for (int h = 0; h < G; ++h) {
-          if (T + 1 < total_steps) gemm0(T + 1, slot_lo(h), slot_lo(h + 1));
-          hop(T, h);
+        const int t = T % steps;  // once per step
+        Slices sl = sl0;
+        sl.start();
+        for (int h = 0; h < G; ++h, sl.step()) {
+          if (T + 1 < total_steps) gemm0(T + 1, sl.lo, sl.hi);
+          hop(T, t, h);
         }
       }
       if (args.prof) {
@@ -619,7 +631,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int T = 0; T < total_steps; ++T) {
         mbar_wait(own_full, T & 1);
         for (int h = 1; h < G; ++h) {
-          const uint32_t dest = (p + h) % G;
+          const uint32_t dest = p + h < (uint32_t)G ? p + h : p + h - G;
           const int R = T * (G - 1) + h - 1;
           if (R >= 2) {
             const int first = (3 - h) <= 0 ? 0 : (3 - h + G - 2) / (G - 1);
@@ -639,18 +651,20 @@ __global__ void __launch_bounds__(256, 1)
     // ===== DSM shuffle, receive side: ack landing, recycle, credit (kMode 0) =====
     if (kDSM && G > 1 && elect_one()) {
       const int total = total_steps * (G - 1);
+      // h = R % (G-1) + 1 and hn = (R+2) % (G-1) + 1 walked incrementally (no division per receive)
+      int h = 1, hn = 2 % (G - 1) + 1;
       for (int R = 0; R < total; ++R) {
         const int b = R & 1;
         const uint32_t ph = (R >> 1) & 1;
         mbar_wait_cluster(recv_full[b], ph);
-        const int h = R % (G - 1) + 1;
-        credit_add_remote(mapa(ack_count, (p + G - h) % G));
+        credit_add_remote(mapa(ack_count, (int)p >= h ? p - h : p + G - h));
         mbar_wait(recv_used[b], ph);
         if (R + 2 < total) {
           mbar_expect_tx(recv_full[b], C::kCHUNK_BYTES);
-          const int hn = (R + 2) % (G - 1) + 1;
-          credit_add_remote(mapa(counter(hn), (p + G - hn) % G));
+          credit_add_remote(mapa(counter(hn), (int)p >= hn ? p - hn : p + G - hn));
         }
+        h = h == G - 1 ? 1 : h + 1;
+        hn = hn == G - 1 ? 1 : hn + 1;
       }
     }
     __syncwarp();  // see warp 0
