@@ -725,7 +725,11 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   a.defer = cfg->ring - 1;
   // split-N reduce-scatter through per-split slabs (else: atomic reduce-add + last-arriver finish)
   a.finish_tma = pair_finish_regions(ch, cfg, rings);
-  a.prefetch = 2;  // measured on a cold L2 (profiles/r01/cold_prefetch.log)
+  // L2 prefetch of weight tiles 2 k-blocks / hops ahead (profiles/r01/cold_prefetch.log): launches of one or two
+  // waves read the weights from HBM and gain (GPT-6.7B -6 us, LLaMA-1B -2 us, OPT M=4096 -1 %); rings of many
+  // units find them in L2, where the prefetch instructions only occupy the TMA unit (OPT M=32768: -2 % without;
+  // r02 s6f / s6g A/Bs)
+  a.prefetch = cfg->units > 2 * rings ? 0 : 2;
   // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
   // FF_VARIANT_NO_KROT restores the common order
   a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;

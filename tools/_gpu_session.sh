@@ -1,6 +1,5 @@
-# scratch driver (r02 session 6e): cold-start weight prefetch A/B
+# scratch driver (r02 session 6h): prefetch rule check + GPU suite
 set -x
-O=gpurun_out/r02s6e; mkdir -p $O
-for i in 1 2 3; do for lib in libff_chain libff_cp8 libff_cp16; do
-  FF_CHAIN_LIB=paper_2512_12949_b200/$lib.so timeout 300 python tools/timeline.py gpt67b llama > $O/t_${lib}_$i.log 2>&1; echo "## $lib"; grep "==\|cfull0" $O/t_${lib}_$i.log | sed 's/{.*}//'
-done; done
+O=gpurun_out/r02s6h; mkdir -p $O
+for i in 1 2; do timeout 300 python tools/timeline.py gpt67b llama opt opt32k > $O/t_$i.log 2>&1; grep "==" $O/t_$i.log | sed 's/{.*}//'; done
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -1 $O/gpu_tests.log
