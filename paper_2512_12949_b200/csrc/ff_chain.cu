@@ -729,7 +729,10 @@ int launch_pair_impl(const ffChainDesc* ch, const ffKernelConfig* cfg, const ffT
   // waves read the weights from HBM and gain (GPT-6.7B -6 us, LLaMA-1B -2 us, OPT M=4096 -1 %); rings of many
   // units find them in L2, where the prefetch instructions only occupy the TMA unit (OPT M=32768: -2 % without;
   // r02 s6f / s6g A/Bs)
-  a.prefetch = cfg->units > 2 * rings ? 0 : 2;
+#ifndef FF_AB_PREFETCH_DIST  // A/B builds only: another prefetch distance
+#define FF_AB_PREFETCH_DIST 2
+#endif
+  a.prefetch = cfg->units > 2 * rings ? 0 : FF_AB_PREFETCH_DIST;
   // staggered GEMM0 k order (measured: GPT-6.7B 118.8 -> 114.7 us, profiles/r01/krot.log);
   // FF_VARIANT_NO_KROT restores the common order
   a.krot = (g_variant & FF_VARIANT_NO_KROT) ? 0 : 1;

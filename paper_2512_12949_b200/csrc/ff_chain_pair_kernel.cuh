@@ -376,7 +376,11 @@ __global__ void __launch_bounds__(256, 1)
           fence_acq_rel_gpu();
           fence_proxy_async_global();
         }
+#ifdef FF_AB_NO_DPREFETCH  // A/B builds only: without the L2 prefetches of hop weight tiles
+        if (false) {
+#else
         if (do_w && args.prefetch && h + args.prefetch < G && (!kQuad || pq == 0)) {  // D rows of a later hop
+#endif
           const int o_pf = p - h - args.prefetch + (p - h - args.prefetch < -G ? 2 * G : p - h - args.prefetch < 0 ? G : 0);
           const int ncol_pf = u.n0 + (st.ns * G + o_pf) * C::kN0;
           for (int kb2 = 0; kb2 < C::kCW / C::BK; ++kb2)
