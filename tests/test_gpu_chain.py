@@ -282,19 +282,22 @@ def test_pair_kernel_serpentine_units_match_oracle(mode):
 # split-N reduce-scatter (11 units of 4 n-steps on 9 rings: 9 whole units + 2 x 4 quarter units),
 # against the oracle with and without it, and bitwise repeatable
 @pytest.mark.parametrize("mode", [0x0, 0x800], ids=["tail-split", "no-tail-split"])
-def test_pair_kernel_tail_split_matches_oracle(mode):
+@pytest.mark.parametrize("case", [("standard_ffn", "relu", 11 * 256, 8192, 512, 2048),   # 2 x 4 quarters of 1 n-step
+                                  ("gated_ffn", "silu", 11 * 256, 8192, 512, 2048)],     # 2 x 4 quarters of 2 n-steps
+                         ids=["standard", "gated"])
+def test_pair_kernel_tail_split_matches_oracle(case, mode):
     torch = _torch()
     from paper_2512_12949_b200 import _native as nat
     from paper_2512_12949_b200 import runtime
 
-    kind, act, m, n, k, l = "standard_ffn", "relu", 11 * 256, 8192, 512, 2048
+    kind, act, m, n, k, l = case
     graph = _graph(kind, act, m, n, k, l)
     host, dev = _inputs(kind, m, n, k, l, seed=17)
     lib = nat.load()
     lib.ff_set_variant(mode)
     try:
         cfg = runtime.lower(graph, None, 148, "pair")
-        assert cfg.units == 11 and cfg.rings == 9 and cfg.steps == 4
+        assert cfg.units == 11 and cfg.rings == 9
         out1 = runtime.launch(graph, cfg, dev).clone()
         out2 = runtime.launch(graph, cfg, dev)
         torch.cuda.synchronize()
