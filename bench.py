@@ -875,6 +875,7 @@ def run_extra(args):
         if name == args.workload:
             continue
         kind, act, m, n, k, l, desc = WORKLOADS[name]
+        time.sleep(args.rest)  # every config from a rested GPU (see the conv note in main)
         try:
             graph = graph_of(name)
             t = make_device_inputs(kind, m, n, k, l, 7, "cuda")
@@ -987,6 +988,8 @@ def main():
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--rest", type=float, default=10.0,
+                    help="seconds of idle GPU before each extra config (clocks recover after sustained load)")
     ap.add_argument("--no-profile-plans", action="store_true",
                     help="take the launch from the shipped M-bin dispatch table instead of ProfileBestFromList "
                          "(keeps an ncu launch list to the timed steps)")
@@ -1025,7 +1028,7 @@ def main():
             # (the FFN configs above) the fused ones ran ~25 % slower for several seconds while
             # cuDNN's did not (tools/conv_time.py: 19.4 vs 15.3 us after a 20 s rest); both arms are
             # timed after the same rest, and interleaved
-            time.sleep(15)
+            time.sleep(args.rest)
             doc["extra"].update(run_extra_conv())
         print(json.dumps(doc), flush=True)
     if world > 1:
