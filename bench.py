@@ -486,6 +486,42 @@ def e2e_pipelined(graph, cfg, tensors, host_a, kind, m, l, steps, dev):
                                         f"one event pair around all {steps} steps"}
 
 
+def copy_bound(host_a, host_e, dev, n=100):
+    """The e2e loop's copy floor on this box: the step's H2D and D2H bytes alone, on two
+    copy streams at once (as the pipelined loop issues them), timed with CUDA events."""
+    import torch
+
+    d_in = torch.empty(host_a.shape, dtype=host_a.dtype, device=dev)
+    d_out = torch.empty(host_e.shape, dtype=host_e.dtype, device=dev)
+    h_out = torch.empty_like(host_e).pin_memory()
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(k):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cur = torch.cuda.current_stream(dev)
+        a.record(cur)
+        s_in.wait_event(a)
+        s_out.wait_event(a)
+        for _ in range(k):
+            with torch.cuda.stream(s_in):
+                d_in.copy_(host_a, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                h_out.copy_(d_out, non_blocking=True)
+        for s in (s_in, s_out):
+            e = torch.cuda.Event()
+            e.record(s)
+            cur.wait_event(e)
+        b.record(cur)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / k
+
+    run(10)
+    ms = run(n)
+    nb = host_a.numel() * host_a.element_size()
+    return {"ms_per_step": round(ms, 4), "gb_per_s_per_direction": round(nb / (ms * 1e-3) / 1e9, 1),
+            "what": f"H2D + D2H of one step's bytes alone on two copy streams, {n} steps, measured after the e2e loop"}
+
+
 def _max_over_ranks(x, dev):
     import torch
     import torch.distributed as dist
@@ -604,6 +640,7 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         e2e_pipe["ms_total"] = _max_over_ranks(e2e_pipe["ms_total"], dev)
     e2e_pipe_value = job_fl * args.steps / (e2e_pipe["ms_total"] * 1e-3) / 1e12
+    copies = copy_bound(host_a, host_e, dev)  # e2e's floor besides the chain (PCIe state varies per box)
 
     # unfused cuBLAS on the same config (eager and CUDA-graph, separate and fused-epilogue activation)
     cub = cublas_unfused(kind, act, tensors, flush, stream, max(min(args.steps, 50), 10))
@@ -658,6 +695,7 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": round(e2e_pipe["ms_total"] / args.steps, 4),
                 "api": "paper_2512_12949_b200.runtime.launch (C ABI ff_chain_launch)",
                 "schedule": e2e_pipe["schedule"],
+                "copy_bound": copies,
                 "serial": {"value": round(e2e_value, 2), "ms_per_step": round(e2e_ms / args.steps, 4),
                            "schedule": "one stream per step: H2D A, chain, D2H E, L2 flushed between steps "
                                        "(outside the per-step events)"}},

@@ -1,6 +1,6 @@
 """Per-CTA phase timeline of a fused-chain launch (diagnostics, GPU box only).
 
-    python tools/timeline.py [gpt67b|llama|opt|gpt2s ...] [x0|x1] [warm] [rings] [variant=0x..]
+    python tools/timeline.py [gpt67b|llama|opt|gpt2s ...] [x0|x1] [warm] [rings] [variant=0x..] [cfg=r,S,nb,lb,x,..]
 
 Every CTA stamps %globaltimer at fixed points (slots 16..31 of the profile
 buffer, ff_set_profile_buffer); this prints min / mean / max per stamp relative
@@ -61,6 +61,13 @@ def main(argv):
     for name in sel:
         keep, ch, kc, t = setup(*SHAPES[name], xchg, lib)
         ws = keep[-1]
+        cfg = next((a.split("=")[1] for a in argv if a.startswith("cfg=")), None)
+        if cfg:  # an explicit launch (all eleven ffKernelConfig fields, e.g. bench.py's "launch")
+            for (fname, _), val in zip(nat.KernelConfig._fields_, cfg.split(",")):
+                setattr(kc, fname, int(val))
+            ws = torch.zeros(lib.ff_chain_workspace_bytes(ctypes.byref(ch), ctypes.byref(kc)) or 256, device='cuda',
+                             dtype=torch.uint8)
+            keep = keep + (ws,)
 
         def f():
             nat.check(lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(kc), ctypes.byref(t), ws.data_ptr(),
