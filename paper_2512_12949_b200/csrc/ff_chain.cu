@@ -791,8 +791,8 @@ bool quad_ok(const ffKernelConfig* cfg, bool gated) {
   if (rings < 2) return false;
   if (g_variant & FF_VARIANT_FORCE_QUAD) return true;  // A/B and tests: quad whenever it can launch
   // one-wave standard FFN (GPT-6.7B): plain pairs -- interleaved A/B over 600 steps each, both orders
-  // (profiles/r02/s5/ab_quad_long.log): -1.0 / -1.2 %; the quad halves the L2 reads of the weights but the
-  // main loop is bound by per-SM operand ingest, not by L2.  Gated FFN (LLaMA-1B: +2.6 % without) and
+  // (profiles/r02/s5/ab_quad_long.log): -1.0 / -1.2 %; the quad halves the L2 reads of the weights, but L2 is
+  // not what bounds the main loop (it runs at the measured per-SM peak).  Gated FFN (LLaMA-1B: +2.6 % without) and
   // multi-unit rings keep quads: OPT M=4096 is 0.8 % faster on 9 plain rings but moves 171.6 instead of
   // 161.7 MB of DRAM (9 rings of C scratch, a 9 + 7 second wave; r02s5v vs r02s5o)
   if (!gated && cfg->units <= pair_rings) return false;

@@ -72,7 +72,8 @@ def main(argv):
         def f():
             nat.check(lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(kc), ctypes.byref(t), ws.data_ptr(),
                                           ws.numel(), None))
-        buf = torch.zeros(kc.grid_ctas * ST + 64, dtype=torch.int64, device='cuda')
+        extra = 64  # CTAs past kc.grid_ctas (GEMM0 helper pairs) stamp rows of their own
+        buf = torch.zeros((kc.grid_ctas + extra) * ST + 64, dtype=torch.int64, device='cuda')
         for _ in range(3):
             f()
         runs = []
@@ -90,9 +91,18 @@ def main(argv):
             lib.ff_set_profile_buffer(None)
             torch.cuda.synchronize()
             w = buf[:kc.grid_ctas * ST].view(kc.grid_ctas, ST).double()
-            runs.append((ea.elapsed_time(eb) * 1e3, w[:, 16:].clone(), w[:, :16].clone()))
+            wx = buf[kc.grid_ctas * ST:(kc.grid_ctas + extra) * ST].view(extra, ST).double()
+            runs.append((ea.elapsed_time(eb) * 1e3, w[:, 16:].clone(), w[:, :16].clone(), wx[:, 16:].clone()))
         runs.sort(key=lambda r: r[0])
-        us, v, cnt = runs[2]
+        us, v, cnt, vx = runs[2]
+        t_zero = v[v[:, 0] > 0][:, 0].min()
+        vx = vx[vx[:, 0] > 0]
+        if vx.numel():  # helper pairs: entry, setup, then one stamp per published chunk
+            relx = (vx - t_zero) / 1e3
+            relx[vx == 0] = float('nan')
+            print(f"   helper CTAs {vx.shape[0]}: chunk publish times (mean over helper CTAs, us):",
+                  " ".join(f"{relx[:, i][~torch.isnan(relx[:, i])].mean().item():6.1f}"
+                           for i in range(2, 14) if (~torch.isnan(relx[:, i])).any()))
         valid = v[:, 0] > 0
         v = v[valid]
         rel = (v - v[:, 0].min()) / 1e3
