@@ -1046,6 +1046,10 @@ def main():
 
     import torch.distributed as dist
 
+    if os.environ.get("FF_BENCH_VARIANT"):  # A/B runs only (tools, profiles): a kernel variant, FF_VARIANT_* bits
+        from paper_2512_12949_b200 import _native
+
+        _native.load().ff_set_variant(int(os.environ["FF_BENCH_VARIANT"], 0))
     if world > 1:
         import torch
 

@@ -790,12 +790,13 @@ bool quad_ok(const ffKernelConfig* cfg, bool gated) {
   int rings = std::min(pair_rings, 4 * table_active_clusters(4, num_sms_cached()) / (2 * cfg->ring)) & ~1;
   if (rings < 2) return false;
   if (g_variant & FF_VARIANT_FORCE_QUAD) return true;  // A/B and tests: quad whenever it can launch
-  // one-wave standard FFN (GPT-6.7B): plain pairs -- interleaved A/B over 600 steps each, both orders
-  // (profiles/r02/s5/ab_quad_long.log): -1.0 / -1.2 %; the quad halves the L2 reads of the weights, but L2 is
-  // not what bounds the main loop (it runs at the measured per-SM peak).  Gated FFN (LLaMA-1B: +2.6 % without) and
-  // multi-unit rings keep quads: OPT M=4096 is 0.8 % faster on 9 plain rings but moves 171.6 instead of
-  // 161.7 MB of DRAM (9 rings of C scratch, a 9 + 7 second wave; r02s5v vs r02s5o)
-  if (!gated && cfg->units <= pair_rings) return false;
+  // Quads wherever they launch.  The chip runs these chains at its board power cap, so the
+  // quad's halved L2 reads of the weights show up as energy per chain and clock, not as feed:
+  // GPT-6.7B sustained (profiles/r02/s6/quad_energy.log) 122.0-123.0 vs 124.1-126.0 us per step at
+  // 3-4 % less energy, bench.py headline 1186 vs 1174 TF/s (bench_ab_quad.log), although an interleaved
+  // A/B -- both variants sharing one power state -- had plain pairs 1 % ahead (s5/ab_quad_long.log).
+  // LLaMA-1B: +2.6 % on plain pairs; OPT M=4096 is 0.8 % faster on 9 plain rings but moves 171.6
+  // instead of 161.7 MB of DRAM (9 rings of C scratch, a 9 + 7 second wave; r02s5v vs r02s5o)
   // quads need an even ring count: when that costs a wave of units (OPT M=32768: 128 units
   // on 8 quad rings = 16 waves vs 9 pair rings = 15), plain pairs win (-2.4 %, A/B)
   const int waves_quad = (cfg->units + rings - 1) / rings, waves_pair = (cfg->units + pair_rings - 1) / pair_rings;
