@@ -841,6 +841,11 @@ __global__ void __launch_bounds__(256, 1)
     // with a single wait: rows of another split's slice go straight to this split's
     // exchange region, rows of this split's slice stay in registers for the sum.
     constexpr int kHalf = kLB / 2;
+    // S >= 4: 128/S rows leave 2 of 8 warps owning the split's rows, so the sum runs on all 256
+    // threads through shared memory (LLaMA-1B, S = 4: tail ~1 us shorter); S = 2 keeps the owners'
+    // register sum, which reads half the shared-memory bytes (GPT-6.7B: ~1.5 us shorter than the
+    // wide sum; profiles/r02/s6/tail_sum_ab.log)
+    const bool wide_sum = S >= 4;
     float ev[kHalf];
     tmem_ld32xn<kHalf / 32>(lane_base + e_col + c_lo, ev);
 #ifndef FF_AB_TAIL  // A/B builds only (results invalid): 1 no region stores, 2 + no partner wait/load, 3 no sum
@@ -851,6 +856,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
       for (int k = 0; k < kHalf / 4; ++k)
         st_global_v4(dst + (size_t)k * 512, __float_as_uint(ev[4 * k]), __float_as_uint(ev[4 * k + 1]),
+                     __float_as_uint(ev[4 * k + 2]), __float_as_uint(ev[4 * k + 3]));
+    } else if (slice == sp && wide_sum) {
+      // own rows into (otherwise unused) slot sp, laid out like the partners' slots: the sum below
+      // then spreads over all 256 threads instead of the 2 * 128/S row owners
+      const uint32_t own = slot0 + sp * (R * kChunks * 16) + (row - sp * R) * 16 + (c_lo / 4) * (R * 16);
+#pragma unroll
+      for (int k = 0; k < kHalf / 4; ++k)
+        st_shared_v4(own + k * (R * 16), __float_as_uint(ev[4 * k]), __float_as_uint(ev[4 * k + 1]),
                      __float_as_uint(ev[4 * k + 2]), __float_as_uint(ev[4 * k + 3]));
     }
     // the barrier orders every thread's region stores before the issuer's
@@ -880,11 +893,43 @@ __global__ void __launch_bounds__(256, 1)
     __syncwarp();  // the issuer's lanes wait for it here, not spinning on e_load (it would starve the polls)
     if (FF_AB_TAIL != 2) mbar_wait(e_load, 0);
     if (issuer && args.prof) args.prof[vcta * FF_PROF_STRIDE + 28] = globaltimer_ns();
-    // sum (deterministic order: own partial, then the partners in split order), cast,
-    // stage bf16.  The own partial is in registers; a warp's 32 rows of one 16-byte
-    // column chunk of a partner slot are 512 contiguous bytes, and the bf16 row stores
-    // are SW128 (8 rows cover all banks).
-    if (slice == sp) {
+    // wide sum: the S slots in split order (deterministic), cast, stage bf16 [kLB/64][R][128 B]
+    // (SW128) for one TMA store: 16-byte items (column chunk c, row rr) of the split's R rows, item
+    // it = c * R + rr, consecutive threads on consecutive rows (512 contiguous bytes per warp and slot)
+    if (wide_sum) {
+      const int n_items = R * kChunks;
+#pragma unroll 1
+      for (int it0 = tid; it0 < n_items; it0 += 4 * 256) {
+        float4 acc[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) acc[q4] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int j = 0; j < S && FF_AB_TAIL != 3; ++j) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            if (it0 + 256 * q4 >= n_items) continue;
+            const float4 f = ld_shared_f4(slot0 + j * (R * kChunks * 16) + (it0 + 256 * q4) * 16);
+            acc[q4].x += f.x;
+            acc[q4].y += f.y;
+            acc[q4].z += f.z;
+            acc[q4].w += f.w;
+          }
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int it = it0 + 256 * q4;
+          if (it >= n_items) continue;
+          const int c = it / R, rr = it - c * R;
+          const int ch = (c % 16) / 2;
+          st_shared_v2(ebuf + (c / 16) * (R * 128) + rr * 128 + ((ch ^ (rr & 7)) << 4) + (c & 1) * 8,
+                       pack2(args.f16, acc[q4].x, acc[q4].y), pack2(args.f16, acc[q4].z, acc[q4].w));
+        }
+      }
+    } else if (slice == sp) {
+      // owners' sum (deterministic order: own partial, then the partners in split order), cast,
+      // stage bf16.  The own partial is in registers; a warp's 32 rows of one 16-byte column
+      // chunk of a partner slot are 512 contiguous bytes, and the bf16 row stores are SW128
+      // (8 rows cover all banks).
       const int rr = row - sp * R;
       const uint32_t part = slot0 + rr * 16 + (c_lo / 4) * (R * 16);
 #pragma unroll
