@@ -1,10 +1,7 @@
-# scratch driver (r02 session 6x): bench with a rest before every extra config
 set -x
-O=gpurun_out/r02s6x; mkdir -p $O
+O=gpurun_out/r02s7; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "pytest rc=$?"
+tail -3 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $O/smoke.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
-python - <<'PY'
-import json
-d=json.loads(open('gpurun_out/r02s6x/bench.json').read().strip().splitlines()[-1])
-print(d['value'], json.dumps(d['fused_vs_cublas'])[:200])
-for k,v in d['extra'].items(): print(k, v.get('fused_ms'), v.get('cublas_best_ms'), v.get('speedup_vs_cublas_best'), v.get('interleaved'))
-PY
+tail -c 1500 $O/bench.json
