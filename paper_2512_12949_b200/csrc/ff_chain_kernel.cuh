@@ -454,6 +454,7 @@ __global__ void __launch_bounds__(256, 1)
             });
           }
           fence_proxy_async_global();
+          FF_STAMP(27);  // every halo tile's C published
           const int hw = args.conv_H * W, img = u.m0 / hw, rem = u.m0 % hw;
           const int nk = args.conv2_k * args.conv2_k * args.conv2_cblk;
           for (int kb2 = 0; kb2 < nk; ++kb2) {
@@ -711,6 +712,7 @@ __global__ void __launch_bounds__(256, 1)
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
+      if (warp == 4 && lane_id() == 0 && T == 0) FF_STAMP(19);  // C chunk 0 drained to shared memory
       tc_fence_before();
       mbar_arrive(c_empty[cb]);
       fence_proxy_async_smem();
@@ -727,6 +729,7 @@ __global__ void __launch_bounds__(256, 1)
           bulk_wait0();
           fence_proxy_async_global();
           st_release_gpu_u32(flag_addr(u, t, (int)p), epoch);
+          if (T == 0) FF_STAMP(20);  // C chunk 0 stored to L2 and its flag released
           mbar_arrive(own_free);
         }
         __syncwarp();  // lanes 1-31 must not spin on the next barrier while the issuer publishes

@@ -1,7 +1,5 @@
-set -x
+# scratch driver (r02 session 7): conv block phase stamps
 O=gpurun_out/r02s7; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "pytest rc=$?"
-tail -3 $O/gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 $O/smoke.log
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
-tail -c 1500 $O/bench.json
+timeout 300 python tools/timeline.py conv_1x1_3x3 conv_c5 x1 counters > $O/timeline_conv_stamps.log 2>&1; echo "rc=$?"
+timeout 300 python tools/timeline.py conv_1x1_3x3 x1 counters warm >> $O/timeline_conv_stamps.log 2>&1; echo "rc=$?"
+cat $O/timeline_conv_stamps.log

@@ -21,7 +21,7 @@ def main(argv):
     lib = _native.load()
     va, vb = int(argv[0], 0), int(argv[1], 0)
     steps = next((int(a.split("=")[1]) for a in argv if a.startswith("steps=")), 200)
-    names = [a for a in argv[2:] if a in bench.WORKLOADS] or ["gpt67b"]
+    names = [a for a in argv[2:] if a in bench.WORKLOADS or a in bench.CONV_WORKLOADS] or ["gpt67b"]
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def flush():
@@ -31,11 +31,24 @@ def main(argv):
     # one workspace large enough for all of them
     runtime._workspace(1 << 30, torch.device("cuda", 0), torch.cuda.current_stream())
     for name in names:
-        kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
-        t = bench.make_device_inputs(kind, m, n, k, l, seed=1, device="cuda")
-        g = bench.graph_of(name, m)
-        cfg = bench.choose_config(name, t, profile=False, m=m, flush=flush)[0]
-        out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
+        if name in bench.CONV_WORKLOADS:  # conv chains: bench.py's shapes, the l2 lowering
+            from paper_2512_12949_b200 import workload as W
+            ic, h, w, oc1, oc2, k1, k2 = bench.CONV_WORKLOADS[name][0]
+            ccfg = W.ConvChainConfig(ic, h, w, oc1, oc2, k1, k2) if k2 == 1 else W.ConvBlockConfig(ic, h, w, oc1, oc2, k1, k2)
+            x = (torch.rand(1, h, w, ic, device="cuda") * 2 - 1).bfloat16()
+            w1 = ((torch.rand(k1, k1, ic, oc1, device="cuda") * 2 - 1) / (k1 * k1 * ic) ** 0.5).bfloat16()
+            w2 = ((torch.rand(*((oc1, oc2) if k2 == 1 else (k2, k2, oc1, oc2)), device="cuda") * 2 - 1) /
+                  (k2 * k2 * oc1) ** 0.5).bfloat16()
+            y = torch.empty(1, h, w, oc2, dtype=torch.bfloat16, device="cuda")
+            kc = runtime.lower_conv(ccfg, 1, "l2")
+            run = lambda: runtime.launch_conv(ccfg, kc, x, w1, w2, out=y)  # noqa: E731
+        else:
+            kind, act, m, n, k, l, _ = bench.WORKLOADS[name]
+            t = bench.make_device_inputs(kind, m, n, k, l, seed=1, device="cuda")
+            g = bench.graph_of(name, m)
+            cfg = bench.choose_config(name, t, profile=False, m=m, flush=flush)[0]
+            out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
+            run = lambda: runtime.launch(g, cfg, t, out=out)  # noqa: E731
         ts = {va: [], vb: []}
         for i in range(steps + 6):
             for v in (va, vb):
@@ -43,7 +56,7 @@ def main(argv):
                 flush()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                runtime.launch(g, cfg, t, out=out)
+                run()
                 b.record()
                 torch.cuda.synchronize()
                 if i >= 6:

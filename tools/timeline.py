@@ -1,6 +1,6 @@
 """Per-CTA phase timeline of a fused-chain launch (diagnostics, GPU box only).
 
-    python tools/timeline.py [gpt67b|llama|opt|gpt2s ...] [x0|x1] [warm] [rings] [variant=0x..] [cfg=r,S,nb,lb,x,..]
+    python tools/timeline.py [gpt67b|llama|opt|gpt2s|conv_c5|conv_1x1_3x3 ...] [x0|x1] [warm] [rings] [variant=0x..] [cfg=r,S,nb,lb,x,..]
 
 Every CTA stamps %globaltimer at fixed points (slots 16..31 of the profile
 buffer, ff_set_profile_buffer); this prints min / mean / max per stamp relative
@@ -50,16 +50,38 @@ def setup(m, n, k, l, act, gated, xchg, lib):
     return (a, b, b1, d, e, ws), ch, kc, t
 
 
+CONVS = {"conv_c5": (64, 56, 56, 64, 256, 3, 1), "conv_1x1_3x3": (256, 56, 56, 64, 64, 1, 3)}
+
+
+def setup_conv(shape, xchg, lib):
+    """A conv chain (bench.py's CONV_WORKLOADS shapes) launched through ff_conv_chain_launch."""
+    from paper_2512_12949_b200 import runtime, workload as W
+    ic, h, w, oc1, oc2, k1, k2 = shape
+    cfg = W.ConvChainConfig(*shape) if k2 == 1 else W.ConvBlockConfig(*shape)
+    x = (torch.rand(1, h, w, ic, device='cuda') * 2 - 1).bfloat16()
+    w1 = ((torch.rand(k1, k1, ic, oc1, device='cuda') * 2 - 1) / (k1 * k1 * ic) ** 0.5).bfloat16()
+    w2 = ((torch.rand(*((oc1, oc2) if k2 == 1 else (k2, k2, oc1, oc2)), device='cuda') * 2 - 1) /
+          (k2 * k2 * oc1) ** 0.5).bfloat16()
+    y = torch.empty(1, h, w, oc2, dtype=torch.bfloat16, device='cuda')
+    kc = runtime.lower_conv(cfg, 1, "dsm" if xchg == 0 else "l2")
+    cd = runtime.conv_desc(cfg, 1)
+    ws = torch.zeros(lib.ff_conv_chain_workspace_bytes(ctypes.byref(cd), ctypes.byref(kc)) or 256,
+                     device='cuda', dtype=torch.uint8)
+    t = nat.Tensors(x.data_ptr(), w1.data_ptr(), None, w2.data_ptr(), y.data_ptr())
+    return (x, w1, w2, y, ws), cd, kc, t
+
+
 def main(argv):
     lib = nat.load()
     flush_buf = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device='cuda')
     sink = torch.empty((), dtype=torch.float32, device='cuda')
-    sel = [a for a in argv if a in SHAPES] or ["gpt67b", "llama"]
+    sel = [a for a in argv if a in SHAPES or a in CONVS] or ["gpt67b", "llama"]
     variant = next((int(a.split("=")[1], 0) for a in argv if a.startswith("variant=")), 0)
     lib.ff_set_variant(variant)
     xchg = 0 if 'x0' in argv else (1 if 'x1' in argv else (3 if 'x3' in argv else 2))
     for name in sel:
-        keep, ch, kc, t = setup(*SHAPES[name], xchg, lib)
+        conv = name in CONVS
+        keep, ch, kc, t = setup_conv(CONVS[name], xchg, lib) if conv else setup(*SHAPES[name], xchg, lib)
         ws = keep[-1]
         cfg = next((a.split("=")[1] for a in argv if a.startswith("cfg=")), None)
         if cfg:  # an explicit launch (all eleven ffKernelConfig fields, e.g. bench.py's "launch")
@@ -70,6 +92,9 @@ def main(argv):
             keep = keep + (ws,)
 
         def f():
+            if conv:
+                return nat.check(lib.ff_conv_chain_launch(ctypes.byref(ch), ctypes.byref(kc), ctypes.byref(t),
+                                                          ws.data_ptr(), ws.numel(), None))
             nat.check(lib.ff_chain_launch(ctypes.byref(ch), ctypes.byref(kc), ctypes.byref(t), ws.data_ptr(),
                                           ws.numel(), None))
         extra = 64  # CTAs past kc.grid_ctas (GEMM0 helper pairs) stamp rows of their own
