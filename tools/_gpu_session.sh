@@ -1,5 +1,6 @@
-# scratch driver (r02 session 7): conv block phase stamps
+# scratch driver (r02 session 7): GPT-2s cold vs warm phases
 O=gpurun_out/r02s7; mkdir -p $O
-timeout 300 python tools/timeline.py conv_1x1_3x3 conv_c5 x1 counters > $O/timeline_conv_stamps.log 2>&1; echo "rc=$?"
-timeout 300 python tools/timeline.py conv_1x1_3x3 x1 counters warm >> $O/timeline_conv_stamps.log 2>&1; echo "rc=$?"
-cat $O/timeline_conv_stamps.log
+timeout 300 python tools/timeline.py gpt2s x0 counters > $O/timeline_gpt2s_coldwarm.log 2>&1
+timeout 300 python tools/timeline.py gpt2s x0 counters warm >> $O/timeline_gpt2s_coldwarm.log 2>&1
+timeout 300 python tools/timeline.py gpt2s x0 counters variant=0x1 >> $O/timeline_gpt2s_coldwarm.log 2>&1
+cat $O/timeline_gpt2s_coldwarm.log
