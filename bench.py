@@ -673,6 +673,7 @@ def run_ours(args, rank, world, local_rank):
                    "global_batch_tokens": m_total if strong else m * world,
                    "parallelism": f"token-sharded x{world} (independent per GPU)",
                    "l2": "flushed between timed steps (256 MiB write)", "launch": cfg.as_dict(),
+                   "bit_reproducible": runtime.is_deterministic(graph, cfg),
                    "plan": cfg_name, "candidates_ms": candidates},
         # the headline comparison: both arms interleaved step by step, so both see the same
         # clocks and power-cap state (a 1000-step fused run and 50-step cuBLAS bursts do not:
@@ -932,7 +933,8 @@ def run_extra(args):
                          "interleaved": {"fused_ms": round(ab[0], 4), "cublas_best_ms": round(ab[1], 4),
                                          "speedup": round(ab[1] / ab[0], 4), "steps": 50},
                          "separate_runs_speedup": round(cub["best_ms"] / ms, 4),
-                         "launch": cfg.as_dict(), "plan": cfg_name, "cublas_unfused": cub,
+                         "launch": cfg.as_dict(), "bit_reproducible": runtime.is_deterministic(graph, cfg),
+                         "plan": cfg_name, "cublas_unfused": cub,
                          "hbm": hbm_table(name, plan)}
         except Exception as exc:  # informative only
             out[name] = {"error": repr(exc)}

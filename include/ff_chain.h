@@ -175,6 +175,15 @@ int ff_chain_run_plan(const ffChainDesc* chain, const ffPlanDesc* plan, const ff
 int ff_chain_launch_debug(const ffChainDesc* chain, const ffKernelConfig* cfg, const ffTensors* t,
                           void* workspace, size_t workspace_bytes, void* c_out, void* stream);
 
+/* *out = 1 when a launch of `cfg` (derived fields recomputed for `chain`, as ff_chain_launch does)
+ * writes a bit-identical E on every run with the same inputs: no N splits, the DSM reduce-scatter
+ * of the splits (FF_XCHG_L2_DSMR), or the CTA-pair kernel's exchange-region finish (one unit per
+ * ring); *out = 0 when the N-split partials meet through TMA reduce-adds, whose order follows the
+ * CTAs' timing (results agree to fp32 rounding, not bitwise).  Host logic only (no GPU work);
+ * describes the planned ring count, i.e. a device where it is co-resident.  Deterministic-mode
+ * selection: paper_2512_12949_b200.runtime.lower(..., deterministic=True). */
+int ff_config_deterministic(const ffChainDesc* chain, const ffKernelConfig* cfg, int32_t num_sms, int32_t* out);
+
 /* Number of CUDA kernels one ff_chain_launch issues (for launch accounting). */
 int ff_chain_kernel_count(const ffChainDesc* chain, const ffKernelConfig* cfg);
 

@@ -1083,6 +1083,32 @@ size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg
   return ws_layout(ch, &cfg).total;
 }
 
+int ff_config_deterministic(const ffChainDesc* ch, const ffKernelConfig* cfg, int32_t num_sms, int32_t* out) {
+  int rc = validate_chain(ch);
+  if (rc) return rc;
+  if (!cfg || !out) return fail(FF_ERR_ARG, "null config or output");
+  if (num_sms <= 0) num_sms = 148;
+  ffKernelConfig c = *cfg;
+  rc = finish_config(ch, &c, num_sms);
+  if (rc) return rc;
+  // Every E element is summed in a fixed order when nothing is summed across CTAs (one N split:
+  // the ring accumulates all of N in one TMEM tile; the pair kernel's tail units meet through the
+  // exchange regions, own partial first, then the partners in split order), when the S splits of a
+  // tile reduce over DSM in split order (FF_XCHG_L2_DSMR), or when the pair kernel finishes its
+  // splits through the exchange regions (one unit per ring, pair_finish_regions).  Otherwise the
+  // split partials meet through TMA reduce-adds into the fp32 zone, whose add order follows the
+  // CTAs' timing.
+  bool det;
+  if (c.n_splits == 1 || c.exchange == FF_XCHG_L2_DSMR)
+    det = true;
+  else if (c.exchange == FF_XCHG_L2_PAIR)
+    det = pair_finish_regions(ch, &c, c.rings);
+  else
+    det = false;  // 1-CTA DSM / L2 rings with N splits (the region finish is an opt-in variant)
+  *out = det ? 1 : 0;
+  return FF_OK;
+}
+
 int ff_chain_kernel_count(const ffChainDesc* ch, const ffKernelConfig* cfg) {
   if (!ch || !cfg) return 0;
   // split-N reduction and the bf16 cast finish inside the chain kernel; only

@@ -99,10 +99,11 @@ class Dispatcher:
             return cls.from_dict(json.load(fh))
 
 
-def candidate_configs(graph, plans=(), labelled: bool = False) -> list:
+def candidate_configs(graph, plans=(), labelled: bool = False, deterministic: bool = False) -> list:
     """Distinct lowerings of the runtime's auto configuration under every
     transport, plus the given plans' lowerings (no GPU needed).  labelled: (cfg,
-    [sources]) pairs, a source per plan / transport that lowers to the config."""
+    [sources]) pairs, a source per plan / transport that lowers to the config.
+    deterministic: only bit-reproducible launches (runtime.is_deterministic)."""
     from . import runtime
 
     seen, out = {}, []
@@ -112,6 +113,8 @@ def candidate_configs(graph, plans=(), labelled: bool = False) -> list:
         try:
             cfg = runtime.lower(graph, plan, 148, x)
         except nat.UnsupportedPlan:
+            continue
+        if deterministic and not runtime.is_deterministic(graph, cfg, 148):
             continue
         key = tuple(int(getattr(cfg, f)) for f in _FIELDS)
         label = f"runtime-auto [{x}]" if plan is None else f"searched #{j} {plan.describe()} [{x}]"
@@ -124,12 +127,15 @@ def candidate_configs(graph, plans=(), labelled: bool = False) -> list:
 
 
 def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT_BINS, iters: int = 10,
-                warmup: int = 3, seed: int = 0, plans_by_m: Optional[dict] = None) -> Dispatcher:
+                warmup: int = 3, seed: int = 0, plans_by_m: Optional[dict] = None,
+                deterministic: bool = False) -> Dispatcher:
     """Profile every candidate launch at each bin's upper edge (L2 flushed
     between timed launches) and keep the fastest: ProfileBestFromList per bin.
     Candidates: the runtime's lowerings under every transport plus the lowerings of
     the reference search's top-K plans for that M (plans_by_m, default: the
-    shipped plans/plan_bins.json -- the offline-search leg, PAPER.md SIV-C3)."""
+    shipped plans/plan_bins.json -- the offline-search leg, PAPER.md SIV-C3).
+    deterministic: bit-reproducible launches only (a reproducible-serving table:
+    every bin's winner writes the same E bits on every run)."""
     import torch
 
     from . import plan_cache, runtime
@@ -155,7 +161,7 @@ def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT
         out = torch.empty((m, l), dtype=torch.bfloat16, device="cuda")
         timed = []
         plans = plans_by_m.get(m, ())
-        for cfg, labels in candidate_configs(graph, plans, labelled=True):
+        for cfg, labels in candidate_configs(graph, plans, labelled=True, deterministic=deterministic):
             for _ in range(warmup):
                 runtime.launch(graph, cfg, tensors, out=out)
             ts = []
@@ -180,7 +186,8 @@ def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT
     return Dispatcher(kind, activation, n, k, l, list(bins), configs,
                       {"device": torch.cuda.get_device_name(), "method": "median of %d cold-L2 launches" % iters,
                        "candidates": "runtime lowerings (pair / l2 / dsm) + lowerings of the reference search's "
-                                     "top-K plans per M bin (plans/plan_bins.json)"})
+                                     "top-K plans per M bin (plans/plan_bins.json)"
+                                     + ("; bit-reproducible launches only" if deterministic else "")})
 
 
 # BASELINE.json families shipped with the package (plans/dispatch/*.json)

@@ -66,15 +66,48 @@ def exchange_name(cfg: nat.KernelConfig) -> str:
     return {v: k for k, v in EXCHANGES.items()}[int(cfg.exchange)]
 
 
+def is_deterministic(graph: ChainGraph, cfg: nat.KernelConfig, num_sms: Optional[int] = None) -> bool:
+    """True when launching ``cfg`` writes a bit-identical E on every run with the same
+    inputs (ff_config_deterministic): no N splits, the DSM reduce-scatter of the splits,
+    or the CTA-pair kernel's exchange-region finish.  Otherwise the N-split partials
+    meet through TMA reduce-adds whose order follows the CTAs' timing."""
+    lib = nat.load()
+    out = ctypes.c_int32(0)
+    nat.check(lib.ff_config_deterministic(ctypes.byref(chain_desc(graph)), ctypes.byref(cfg),
+                                          num_sms if num_sms is not None else 148, ctypes.byref(out)))
+    return bool(out.value)
+
+
 def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optional[int] = None,
-          exchange: str = "auto") -> nat.KernelConfig:
+          exchange: str = "auto", deterministic: bool = False) -> nat.KernelConfig:
     """Physical launch configuration for (graph, plan).  plan=None lets the
     runtime choose the hardware-shaped configuration; ``exchange`` picks the
     shuffle transport: "dsm" (thread-block cluster, distributed shared memory),
     "l2" (TMA through an L2-resident scratch), "pair" (L2 transport, CTA-pair
     cta_group::2 kernel), "l2dsm" (L2 ring; the N splits of every E tile form a
     thread-block cluster and reduce their partials over DSM) or "auto" (first of
-    pair, l2, dsm that supports it)."""
+    pair, l2, dsm that supports it).
+
+    deterministic=True: only launches whose E is bit-identical run to run
+    (is_deterministic).  "auto" then returns the first of pair, l2dsm, l2, dsm
+    that qualifies; an explicit transport whose lowering sums split partials by
+    reduce-adds raises UnsupportedPlan."""
+    if deterministic:
+        if exchange == "auto":
+            for candidate in ("pair", "l2dsm", "l2", "dsm"):
+                try:
+                    cfg = lower(graph, plan, num_sms, candidate)
+                except nat.UnsupportedPlan:
+                    continue
+                if is_deterministic(graph, cfg, num_sms):
+                    return cfg
+            raise nat.UnsupportedPlan("no bit-reproducible lowering (every transport sums N-split partials by "
+                                      "reduce-adds); pass an explicit one-split config to launch()")
+        cfg = lower(graph, plan, num_sms, exchange)
+        if not is_deterministic(graph, cfg, num_sms):
+            raise nat.UnsupportedPlan(f"the {exchange} lowering ({cfg.as_dict()}) sums its N-split partials by "
+                                      "reduce-adds: not bit-reproducible (deterministic=True)")
+        return cfg
     if exchange == "auto":
         last = None
         for candidate in ("pair", "l2", "dsm"):
@@ -198,9 +231,10 @@ def launch(graph: ChainGraph, cfg: nat.KernelConfig, tensors: dict, out=None, st
 
 
 def run(graph: ChainGraph, plan: Optional[FusionPlan], tensors: dict, out=None, stream=None,
-        exchange: str = "auto"):
-    """Execute the chain under ``plan`` on the current GPU; returns E (bf16)."""
-    return launch(graph, lower(graph, plan, _num_sms(), exchange), tensors, out=out, stream=stream)
+        exchange: str = "auto", deterministic: bool = False):
+    """Execute the chain under ``plan`` on the current GPU; returns E (bf16).
+    deterministic=True restricts the lowering to bit-reproducible launches (see lower)."""
+    return launch(graph, lower(graph, plan, _num_sms(), exchange, deterministic), tensors, out=out, stream=stream)
 
 
 def kernel_launches(graph: ChainGraph, cfg: nat.KernelConfig) -> int:

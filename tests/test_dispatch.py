@@ -45,3 +45,18 @@ def test_dispatch_ragged_m_matches_oracle(name, m):
     got = out.float().cpu().numpy()
     ref = oracle.dense_chain(kind, t.activation, host, bf16_intermediate=True)
     assert np.isfinite(got).all() and oracle.max_relative_error(got, ref) <= 1e-2
+
+
+def test_deterministic_candidates_are_reproducible():
+    """A reproducible-serving table draws only on bit-reproducible launches (host logic)."""
+    from paper_2512_12949_b200 import runtime
+
+    for name, m in (("gpt2s", 512), ("llama1b", 512), ("opt13b", 4096)):
+        kind, act, n, k, l = dispatch.FAMILIES[name]
+        g = dispatch.family_graph(kind, act, m, n, k, l)
+        every = dispatch.candidate_configs(g)
+        det = dispatch.candidate_configs(g, deterministic=True)
+        assert det and len(det) <= len(every)
+        assert all(runtime.is_deterministic(g, c) for c in det)
+    g = dispatch.family_graph("standard_ffn", "gelu", 512, 3072, 768, 768)
+    assert len(dispatch.candidate_configs(g, deterministic=True)) < len(dispatch.candidate_configs(g))

@@ -549,3 +549,35 @@ def test_cuda_graph_capture_replays_the_chain(exchange, case):
             g.replay()
             st.synchronize()
             _check(kind, act, dict(host, A=new_a), out)
+
+
+# deterministic mode (runtime.lower(..., deterministic=True), ff_config_deterministic): the
+# selected launch matches the oracle and writes a bit-identical E on repeated runs, also when
+# other launches (the reduce-add lowerings) run in between and perturb the timing
+@pytest.mark.parametrize("case", [("standard_ffn", "gelu", 512, 3072, 768, 768),
+                                  ("gated_ffn", "silu", 512, 8192, 2048, 2048),
+                                  ("standard_ffn", "relu", 1024, 4096, 1024, 1024),
+                                  ("standard_ffn", "relu", 200, 768, 256, 768)],
+                         ids=["gpt2s", "llama1b", "std-1024", "ragged-m"])
+@pytest.mark.parametrize("exchange", ["auto", "l2dsm"])
+def test_deterministic_mode_matches_oracle_and_repeats_bitwise(case, exchange):
+    torch = _torch()
+    from paper_2512_12949_b200 import _native as nat
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    host, dev = _inputs(kind, m, n, k, l, seed=23)
+    try:
+        cfg = runtime.lower(graph, None, 148, exchange, deterministic=True)
+    except nat.UnsupportedPlan:
+        pytest.skip(f"no bit-reproducible {exchange} lowering for this shape")
+    assert runtime.is_deterministic(graph, cfg)
+    first = runtime.launch(graph, cfg, dev).clone()
+    _check(kind, act, host, first)
+    other = runtime.lower(graph, None, 148, "l2")
+    for _ in range(4):
+        runtime.launch(graph, other, dev)  # a reduce-add lowering in between
+        again = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+        assert torch.equal(first, again), "deterministic launch changed its result"

@@ -193,3 +193,29 @@ def test_run_plan_rejects_plans_without_lowering(lib):
     assert b"gated lowering" in lib.ff_last_error()
     with pytest.raises(PlanError):
         nat.check(rc)
+
+
+def test_deterministic_predicate_and_selection(lib):
+    """ff_config_deterministic: one N split, the DSM reduce-scatter and the pair kernel's region
+    finish are bit-reproducible; 1-CTA rings that reduce-add their splits are not.  lower(...,
+    deterministic=True) picks a reproducible launch or refuses (host logic, no GPU)."""
+    gpt2s = W.build_standard_ffn(W.DimensionSpec(512, 3072, 768, 768, 2), "relu")
+    llama = W.build_gated_ffn(W.DimensionSpec(512, 8192, 2048, 2048, 2))
+    opt = W.build_standard_ffn(W.DimensionSpec(4096, 8192, 2048, 2048, 2), "relu")
+    for g in (gpt2s, llama):
+        l2 = runtime.lower(g, None, 148, "l2")
+        assert l2.n_splits > 1 and not runtime.is_deterministic(g, l2)
+        assert runtime.is_deterministic(g, runtime.lower(g, None, 148, "l2dsm"))
+        assert runtime.is_deterministic(g, runtime.lower(g, None, 148, "pair"))
+        with pytest.raises(nat.UnsupportedPlan):
+            runtime.lower(g, None, 148, "l2", deterministic=True)
+        det = runtime.lower(g, None, 148, "auto", deterministic=True)
+        assert runtime.is_deterministic(g, det)
+    one = runtime.lower(opt, None, 148, "l2")
+    assert one.n_splits == 1 and runtime.is_deterministic(opt, one)
+    # a multi-unit pair launch with N splits finishes by reduce-adds
+    multi = runtime.lower(opt, None, 148, "pair")
+    multi.n_splits = 2
+    assert not runtime.is_deterministic(opt, multi)
+    out = ctypes.c_int32(7)
+    assert lib.ff_config_deterministic(ctypes.byref(runtime.chain_desc(opt)), None, 148, ctypes.byref(out)) == nat.FF_ERR_ARG
