@@ -175,6 +175,10 @@ int ff_chain_run_plan(const ffChainDesc* chain, const ffPlanDesc* plan, const ff
 int ff_chain_launch_debug(const ffChainDesc* chain, const ffKernelConfig* cfg, const ffTensors* t,
                           void* workspace, size_t workspace_bytes, void* c_out, void* stream);
 
+/* Validate an explicit launch (ring, n_splits, nb, lb, exchange) for `chain` and fill its derived
+ * fields (m_tiles, l_clusters, steps, units, rings, grid_ctas) as ff_chain_launch will; no GPU work. */
+int ff_config_finish(const ffChainDesc* chain, int32_t num_sms, ffKernelConfig* cfg);
+
 /* *out = 1 when a launch of `cfg` (derived fields recomputed for `chain`, as ff_chain_launch does)
  * writes a bit-identical E on every run with the same inputs: no N splits, the DSM reduce-scatter
  * of the splits (FF_XCHG_L2_DSMR), or the CTA-pair kernel's exchange-region finish (one unit per

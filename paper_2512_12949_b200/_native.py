@@ -42,6 +42,7 @@ EXPORTS = (
     "ff_chain_launch_debug",
     "ff_chain_kernel_count",
     "ff_config_deterministic",
+    "ff_config_finish",
     "ff_set_profile_buffer",
     "ff_set_variant",
     "ff_last_error",
@@ -158,6 +159,7 @@ def load(path: str = LIB_PATH):
         lib.ff_chain_kernel_count.argtypes = [P(ChainDesc), P(KernelConfig)]
         lib.ff_config_deterministic.argtypes = [P(ChainDesc), P(KernelConfig), ctypes.c_int32,
                                                 P(ctypes.c_int32)]
+        lib.ff_config_finish.argtypes = [P(ChainDesc), ctypes.c_int32, P(KernelConfig)]
         lib.ff_set_profile_buffer.argtypes = [ctypes.c_void_p]
         lib.ff_set_variant.argtypes = [ctypes.c_uint32]
         lib.ff_conv_chain_desc.argtypes = [P(ConvDesc), P(ChainDesc)]

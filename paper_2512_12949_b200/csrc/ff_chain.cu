@@ -1083,6 +1083,17 @@ size_t ff_chain_workspace_bytes(const ffChainDesc* ch, const ffKernelConfig* cfg
   return ws_layout(ch, &cfg).total;
 }
 
+int ff_config_finish(const ffChainDesc* ch, int32_t num_sms, ffKernelConfig* cfg) {
+  int rc = validate_chain(ch);
+  if (rc) return rc;
+  if (!cfg) return fail(FF_ERR_ARG, "null config");
+  ffKernelConfig c = *cfg;
+  rc = finish_config(ch, &c, num_sms > 0 ? num_sms : 148);
+  if (rc) return rc;
+  *cfg = c;
+  return FF_OK;
+}
+
 int ff_config_deterministic(const ffChainDesc* ch, const ffKernelConfig* cfg, int32_t num_sms, int32_t* out) {
   int rc = validate_chain(ch);
   if (rc) return rc;

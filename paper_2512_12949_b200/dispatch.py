@@ -109,21 +109,42 @@ def candidate_configs(graph, plans=(), labelled: bool = False, deterministic: bo
     seen, out = {}, []
     xs = ("pair", "l2", "dsm", "l2dsm")
     sources = [(None, -1, x) for x in xs] + [(p, j, x) for j, p in enumerate(plans) for x in xs]
+    sources += [(cfg, -2, "l2dsm") for cfg in runtime.reproducible_configs(graph, 148)]
     for plan, j, x in sources:
-        try:
-            cfg = runtime.lower(graph, plan, 148, x)
-        except nat.UnsupportedPlan:
-            continue
+        if j == -2:  # an explicit reproducible launch (runtime.reproducible_configs)
+            cfg, plan = plan, None
+        else:
+            try:
+                cfg = runtime.lower(graph, plan, 148, x)
+            except nat.UnsupportedPlan:
+                continue
         if deterministic and not runtime.is_deterministic(graph, cfg, 148):
             continue
         key = tuple(int(getattr(cfg, f)) for f in _FIELDS)
-        label = f"runtime-auto [{x}]" if plan is None else f"searched #{j} {plan.describe()} [{x}]"
+        label = (f"reproducible ring {cfg.ring} x {cfg.n_splits} splits nb {cfg.nb} lb {cfg.lb} [{x}]" if j == -2
+                 else f"runtime-auto [{x}]" if plan is None else f"searched #{j} {plan.describe()} [{x}]")
         if key in seen:
             seen[key][1].append(label)
         else:
             seen[key] = (cfg, [label])
             out.append(seen[key])
     return out if labelled else [c for c, _ in out]
+
+
+TIE = 1.01  # a bit-reproducible launch within 1 % of the fastest wins (run-to-run identical E for free)
+
+
+def pick_reproducible(graph, timed):
+    """timed: [(ms, cfg, ...)] sorted by ms.  The fastest entry, unless a bit-reproducible
+    launch (runtime.is_deterministic) is within TIE of it: then that one."""
+    from . import runtime
+
+    for entry in timed:
+        if entry[0] > timed[0][0] * TIE:
+            break
+        if runtime.is_deterministic(graph, entry[1], 148):
+            return entry
+    return timed[0]
 
 
 def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT_BINS, iters: int = 10,
@@ -175,7 +196,7 @@ def build_table(kind: str, activation: str, n: int, k: int, l: int, bins=DEFAULT
                 ts.append(a.elapsed_time(b))
             timed.append((sorted(ts)[len(ts) // 2], cfg, labels))
         timed.sort(key=lambda x: x[0])
-        ms, best, labels = timed[0]
+        ms, best, labels = pick_reproducible(graph, timed)
         entry = {f: int(getattr(best, f)) for f in _FIELDS}
         entry["ms"] = round(ms, 5)
         entry["candidates"] = len(timed)

@@ -66,6 +66,36 @@ def exchange_name(cfg: nat.KernelConfig) -> str:
     return {v: k for k, v in EXCHANGES.items()}[int(cfg.exchange)]
 
 
+def explicit_config(graph: ChainGraph, ring: int, n_splits: int, nb: int, lb: int, exchange: str,
+                    num_sms: Optional[int] = None) -> nat.KernelConfig:
+    """An explicit physical launch, validated and completed (ff_config_finish);
+    raises UnsupportedPlan when no kernel runs it."""
+    lib = nat.load()
+    cfg = nat.KernelConfig()
+    cfg.ring, cfg.n_splits, cfg.nb, cfg.lb, cfg.exchange = ring, n_splits, nb, lb, EXCHANGES[exchange]
+    nat.check(lib.ff_config_finish(ctypes.byref(chain_desc(graph)), num_sms if num_sms is not None else 148,
+                                   ctypes.byref(cfg)))
+    return cfg
+
+
+def reproducible_configs(graph: ChainGraph, num_sms: Optional[int] = None) -> list:
+    """Explicit DSM reduce-scatter launches (FF_XCHG_L2_DSMR: the S splits of an E tile are
+    one cluster and sum in split order) over the E slice widths and chunk widths the 1-CTA
+    kernels run -- bit-reproducible alternatives to the reduce-add split lowerings (GPT-2s:
+    ring 6 x 4 splits ties the fastest reduce-add launch, profiles/r02/s5/sweep_final.log)."""
+    out = []
+    for lb in (256, 128):
+        if graph.dims.l % lb:
+            continue
+        for s in (2, 4, 8):
+            for nb in (128, 64):
+                try:
+                    out.append(explicit_config(graph, graph.dims.l // lb, s, nb, lb, "l2dsm", num_sms))
+                except nat.FusePlanError:
+                    continue
+    return out
+
+
 def is_deterministic(graph: ChainGraph, cfg: nat.KernelConfig, num_sms: Optional[int] = None) -> bool:
     """True when launching ``cfg`` writes a bit-identical E on every run with the same
     inputs (ff_config_deterministic): no N splits, the DSM reduce-scatter of the splits,
@@ -101,6 +131,9 @@ def lower(graph: ChainGraph, plan: Optional[FusionPlan] = None, num_sms: Optiona
                     continue
                 if is_deterministic(graph, cfg, num_sms):
                     return cfg
+            rc = reproducible_configs(graph, num_sms) if plan is None else []
+            if rc:
+                return rc[0]
             raise nat.UnsupportedPlan("no bit-reproducible lowering (every transport sums N-split partials by "
                                       "reduce-adds); pass an explicit one-split config to launch()")
         cfg = lower(graph, plan, num_sms, exchange)

@@ -219,3 +219,18 @@ def test_deterministic_predicate_and_selection(lib):
     assert not runtime.is_deterministic(opt, multi)
     out = ctypes.c_int32(7)
     assert lib.ff_config_deterministic(ctypes.byref(runtime.chain_desc(opt)), None, 148, ctypes.byref(out)) == nat.FF_ERR_ARG
+
+
+def test_config_finish_and_reproducible_configs(lib):
+    """ff_config_finish completes an explicit launch like ff_chain_launch will; the explicit DSM
+    reduce-scatter launches are all bit-reproducible and co-resident (host logic, no GPU)."""
+    g = W.build_standard_ffn(W.DimensionSpec(512, 3072, 768, 768, 2), "gelu")
+    cfg = runtime.explicit_config(g, 6, 4, 128, 128, "l2dsm")
+    assert (cfg.m_tiles, cfg.l_clusters, cfg.steps, cfg.units, cfg.rings, cfg.grid_ctas) == (4, 1, 1, 16, 16, 96)
+    with pytest.raises(nat.UnsupportedPlan):
+        runtime.explicit_config(g, 6, 8, 128, 128, "l2dsm")  # 192 CTAs in clusters of 8: not co-resident
+    with pytest.raises(nat.UnsupportedPlan):
+        runtime.explicit_config(g, 5, 2, 128, 128, "l2")  # 5 x 128 columns do not tile l = 768
+    rc = runtime.reproducible_configs(g)
+    assert rc and all(runtime.is_deterministic(g, c) and c.grid_ctas <= 148 for c in rc)
+    assert any((c.ring, c.n_splits, c.nb, c.lb) == (6, 4, 128, 128) for c in rc)
