@@ -1,12 +1,15 @@
-# scratch driver (r02 session 7): rebuild the shipped M-bin tables with the reproducible candidates, bench, suite
+# scratch driver (r02 session 7): batched TMEM drains in the 1-CTA kernels vs the 16-column loop (A build)
 O=gpurun_out/r02s7; mkdir -p $O
-cp -r paper_2512_12949_b200/plans/dispatch $O/dispatch_before
-( time timeout 1500 python -m paper_2512_12949_b200.dispatch ) > $O/dispatch_build.log 2>&1; echo "dispatch rc=$?"; tail -6 $O/dispatch_build.log
-mkdir -p $O/dispatch_after && cp paper_2512_12949_b200/plans/dispatch/*.json $O/dispatch_after/
-timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests3.log 2>&1; echo "pytest rc=$?"; tail -2 $O/gpu_tests3.log
-timeout 900 python bench.py > $O/bench3.json 2> $O/bench3.err; echo "bench rc=$?"
-python -c "
-import json; d=json.loads(open('$O/bench3.json').read().strip().splitlines()[-1])
-print(d['value'], d['config']['bit_reproducible'], d['config']['plan'][:80], d['fused_vs_cublas']['speedup'], d['e2e']['value'])
-for k,v in d['extra'].items(): print(k, v.get('bit_reproducible'), str(v.get('plan'))[:70], v.get('interleaved'))
-"
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests_drain.log 2>&1; echo "pytest rc=$?"; tail -2 $O/gpu_tests_drain.log
+for r in 1 2; do
+ for lib in libff_ab_drain16.so libff_chain.so; do
+  echo "== $lib round $r"
+  FF_CHAIN_LIB=paper_2512_12949_b200/$lib timeout 600 python tools/ab_variant.py 0x0 0x0 gpt2s llama1b conv_1x1_3x3 conv_c5 steps=200 2>&1 | grep variant
+ done
+done > $O/ab_drain.log 2>&1
+cat $O/ab_drain.log
+for lib in libff_ab_drain16.so libff_chain.so; do
+  FF_CHAIN_LIB=paper_2512_12949_b200/$lib timeout 300 python tools/timeline.py gpt2s x0 counters 2>&1 | grep -E "==|cfull0|drained0|E_start|E_staged|E_fin"
+  FF_CHAIN_LIB=paper_2512_12949_b200/$lib timeout 300 python tools/timeline.py gpt2s x3 cfg=6,4,128,128,3,4,1,1,16,16,96 2>&1 | grep -E "==|cfull0|drained0|E_start|E_staged|E_fin"
+done > $O/timeline_drain.log 2>&1
+cat $O/timeline_drain.log
