@@ -56,6 +56,9 @@ def test_simulate_runs_the_fused_kernel_and_verifies(capsys, tmp_path):
     assert doc["verify"]["max_rel_error"] <= 1e-2
     rc, doc = _run(capsys, ["run", "--dims", "512,8192,2048,2048", "--gated", "--iters", "5"])
     assert rc == 0 and doc["tflops"] > 100 and doc["exchange"] in ("pair", "l2", "dsm")
+    rc, doc = _run(capsys, ["run", "--dims", "512,3072,768,768", "--activation", "gelu", "--exchange", "l2dsm",
+                            "--deterministic", "--iters", "5"])
+    assert rc == 0 and doc["bit_reproducible"] and doc["exchange"] == "l2dsm"
 
 
 def test_export_dot_plan_and_launch(capsys, tmp_path):
