@@ -60,3 +60,25 @@ def test_deterministic_candidates_are_reproducible():
         assert all(runtime.is_deterministic(g, c) for c in det)
     g = dispatch.family_graph("standard_ffn", "gelu", 512, 3072, 768, 768)
     assert len(dispatch.candidate_configs(g, deterministic=True)) < len(dispatch.candidate_configs(g))
+
+
+@pytest.mark.gpu
+def test_reproducible_table_build_and_run():
+    """build_table(deterministic=True) profiles only bit-reproducible launches; its run() repeats bitwise."""
+    import torch
+
+    from paper_2512_12949_b200 import runtime
+
+    t = dispatch.build_table("standard_ffn", "gelu", 3072, 768, 768, bins=(128, 512), iters=3, warmup=1,
+                             plans_by_m={}, deterministic=True)
+    for b in t.bins:
+        assert runtime.is_deterministic(t.graph_for(b), t.config_for(b))
+    m = 300
+    host = {k: oracle.round_bf16(v) for k, v in oracle.make_inputs("standard_ffn", m, 3072, 768, 768, seed=4).items()}
+    dev = {k: torch.from_numpy(v).cuda().to(torch.bfloat16) for k, v in host.items()}
+    first = t.run(dev).clone()
+    again = t.run(dev)
+    torch.cuda.synchronize()
+    assert torch.equal(first, again)
+    ref = oracle.dense_chain("standard_ffn", "gelu", host, bf16_intermediate=True)
+    assert oracle.max_relative_error(first.float().cpu().numpy(), ref) <= 1e-2
