@@ -82,3 +82,16 @@ def test_reproducible_table_build_and_run():
     assert torch.equal(first, again)
     ref = oracle.dense_chain("standard_ffn", "gelu", host, bf16_intermediate=True)
     assert oracle.max_relative_error(first.float().cpu().numpy(), ref) <= 1e-2
+
+
+def test_pick_reproducible_tie_rule():
+    """The fastest launch wins unless a bit-reproducible one is within dispatch.TIE of it (host logic)."""
+    from paper_2512_12949_b200 import runtime
+
+    g = dispatch.family_graph("standard_ffn", "gelu", 512, 3072, 768, 768)
+    fast = runtime.lower(g, None, 148, "dsm")           # N splits summed by reduce-adds
+    det = runtime.explicit_config(g, 6, 4, 128, 128, "l2dsm")
+    assert not runtime.is_deterministic(g, fast) and runtime.is_deterministic(g, det)
+    assert dispatch.pick_reproducible(g, [(1.000, fast, "a"), (1.005, det, "b")])[1] is det
+    assert dispatch.pick_reproducible(g, [(1.000, fast, "a"), (1.050, det, "b")])[1] is fast
+    assert dispatch.pick_reproducible(g, [(1.000, det, "b"), (1.001, fast, "a")])[1] is det
