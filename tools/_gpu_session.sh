@@ -1,8 +1,7 @@
-# scratch driver (r02 session 7): the N-rank bench path (2 ranks sharing the one GPU) at HEAD
+# scratch driver (r02 session 7): final checks at HEAD -- GPU suite, smoke, smoke under ncu (as the driver runs it)
 O=gpurun_out/r02s7; mkdir -p $O
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 \
-  bench.py --gpus 2 --steps 50 --warmup 3 --no-extra --no-cpu > $O/bench_n2.json 2> $O/bench_n2.err; echo "rc=$?"
-tail -c 600 $O/bench_n2.json; tail -3 $O/bench_n2.err
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29532 \
-  bench.py --impl reference --gpus 2 --steps 2 --warmup 3 > $O/bench_n2_ref.json 2> $O/bench_n2_ref.err; echo "ref rc=$?"
-tail -c 300 $O/bench_n2_ref.json
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests_final.log 2>&1; echo "pytest rc=$?"; tail -1 $O/gpu_tests_final.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke_final.log 2>&1; echo "smoke rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_smoke_final.csv \
+  python -c "import __graft_entry__ as g; g.smoke()" > $O/ncu_smoke_final.log 2>&1; echo "ncu smoke rc=$?"
+grep -c ff_chain $O/ncu_smoke_final.csv; grep "ff_chain" $O/ncu_smoke_final.csv | awk -F'","' '{print $5, $NF}' | cut -c1-120
