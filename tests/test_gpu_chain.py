@@ -581,3 +581,26 @@ def test_deterministic_mode_matches_oracle_and_repeats_bitwise(case, exchange):
         again = runtime.launch(graph, cfg, dev)
         torch.cuda.synchronize()
         assert torch.equal(first, again), "deterministic launch changed its result"
+
+
+@pytest.mark.parametrize("case", [("standard_ffn", "gelu", 512, 3072, 768, 768),
+                                  ("gated_ffn", "silu", 256, 2048, 512, 512)], ids=["gpt2s", "gated-small"])
+def test_deterministic_mode_fp16_repeats_bitwise(case):
+    """fp16 storage through the reproducible launches: the oracle bound and bitwise repeats."""
+    torch = _torch()
+    from paper_2512_12949_b200 import runtime
+
+    kind, act, m, n, k, l = case
+    graph = _graph(kind, act, m, n, k, l)
+    raw = oracle.make_inputs(kind, m, n, k, l, seed=8)
+    scale = {"A": 1.0, "B": k ** -0.5, "B0": k ** -0.5, "B1": k ** -0.5, "D": n ** -0.5}
+    host = {name: oracle.round_f16(v * scale[name]) for name, v in raw.items()}
+    dev = {name: torch.from_numpy(v).cuda().to(torch.float16) for name, v in host.items()}
+    for cfg in runtime.reproducible_configs(graph)[:3] + [runtime.lower(graph, None, 148, "auto", deterministic=True)]:
+        assert runtime.is_deterministic(graph, cfg)
+        first = runtime.launch(graph, cfg, dev).clone()
+        again = runtime.launch(graph, cfg, dev)
+        torch.cuda.synchronize()
+        assert first.dtype == torch.float16 and torch.equal(first, again), cfg.as_dict()
+        got = first.float().cpu().numpy()
+        assert oracle.max_relative_error(got, oracle.dense_chain(kind, act, host, f16_intermediate=True)) <= TOL
